@@ -1,0 +1,195 @@
+/*
+ * heat1d.h -- C ABI of libheat1d, a B200 (sm_100a) implementation of the
+ * explicit forward-Euler, 3-point finite-difference update of the 1D heat
+ * equation on a periodic ring of fp64 cells (arxiv 2307.01117, §2):
+ *
+ *     u(t+dt, x_i) = u(t,x_i) + dt*k*(u(t,x_{i-1}) - 2u(t,x_i) + u(t,x_{i+1})) / D
+ *
+ * (Eq. 2), grid x_i = i*dx, i = 0..N-1,
+ * periodic boundary u(t,x) = u(t,L+x), D = dx^2 by default
+ * (reading c1; the literal "2h" of PAPER.md:68 is HEAT1D_DEN_PAPER_2DX).
+ * The ring is cut into np partitions of nx cells (N = nx*np) whose ghost
+ * zones are exchanged between neighbours; here the ring is cut
+ * into contiguous slabs, one per GPU rank, exchanging depth-T halos every T
+ * steps (NCCL send/recv), and each GPU advances T steps per HBM pass.
+ *
+ * Conventions
+ *   - All functions return int status (heat1d_status) unless stated.
+ *   - Pointers are plain host (pageable or pinned) or device pointers; copies
+ *     use cudaMemcpyDefault (unified addressing).  No torch types cross this
+ *     boundary.
+ *   - Arithmetic (reading c3): r = (k*dt)/(dx*dx) once on the host;
+ *     every update is v = b + r*((a - 2b) + c), a=u[i-1], b=u[i], c=u[i+1],
+ *     binary64 RNE.  HEAT1D_MODE_MATCHED evaluates exactly that sequence (the
+ *     result is bitwise independent of T, np, the slab count and the GPU
+ *     count, and bitwise equal to the CPU oracle); HEAT1D_MODE_FAST contracts
+ *     the last multiply-add into one fma (error <= 1e-12*max|u0|*nt).
+ *   - Threading: one host thread per handle.  A handle whose CUDA or NCCL
+ *     call failed is "poisoned": every later call except heat1d_destroy
+ *     returns the same error.
+ */
+#ifndef HEAT1D_H
+#define HEAT1D_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HEAT1D_VERSION 10000 /* 1.0.0 */
+
+#if defined(__GNUC__)
+#define HEAT1D_API __attribute__((visibility("default")))
+#else
+#define HEAT1D_API
+#endif
+
+typedef struct heat1d_s *heat1d_t; /* opaque; one per rank (per GPU) */
+
+typedef enum {
+    HEAT1D_OK = 0,
+    HEAT1D_EINVAL = 1,       /* bad argument: sizes, non-finite k/dt/dx, count mismatch, ranks */
+    HEAT1D_EUNSTABLE = 2,    /* r > 1/2 without allow_unstable               */
+    HEAT1D_ESTATE = 3,       /* run/get before set_initial, or use of a poisoned handle         */
+    HEAT1D_ENOMEM = 4,       /* device allocation failed                                        */
+    HEAT1D_ECUDA = 5,        /* CUDA runtime / kernel error (handle poisoned)                   */
+    HEAT1D_ENCCL = 6,        /* NCCL error (handle poisoned)                                    */
+    HEAT1D_EUNSUPPORTED = 7  /* valid request this build does not implement                     */
+} heat1d_status;
+
+enum { HEAT1D_MODE_MATCHED = 0, HEAT1D_MODE_FAST = 1 };
+enum { HEAT1D_DEN_DX2 = 0, HEAT1D_DEN_PAPER_2DX = 1 };
+enum {
+    HEAT1D_KERNEL_AUTO = 0,   /* temporal-blocked TMA pass kernel (K2)                        */
+    HEAT1D_KERNEL_NAIVE = 1   /* one step per launch, modular indexing (K1; T forced to 1)    */
+};
+
+#define HEAT1D_T_MAX 32
+
+/* Options.  Always initialise with heat1d_opts_default(); `size` versions the struct. */
+typedef struct {
+    uint32_t size;          /* = sizeof(heat1d_opts)                                        */
+    int32_t device;         /* CUDA ordinal; -1 = the calling thread's current device       */
+    int32_t rank, nranks;   /* position in the GPU ring; (0,1) = single GPU                 */
+    const void *nccl_id;    /* 128-byte ncclUniqueId from heat1d_get_unique_id on rank 0;
+                               required iff nranks > 1                                      */
+    int32_t T;              /* steps fused per HBM pass = halo depth, 1..HEAT1D_T_MAX;
+                               0 = auto (chosen per arithmetic mode)          */
+    int32_t mode;           /* HEAT1D_MODE_*                                                */
+    int32_t denominator;    /* HEAT1D_DEN_*                                                 */
+    int32_t allow_unstable; /* nonzero: accept r > 1/2                                      */
+    int32_t virtual_slabs;  /* >= 1; with nranks == 1, split the ring into this many slabs on
+                               ONE device that exchange halos by device copies -- the exact
+                               multi-GPU schedule with the transport replaced (test harness) */
+    int32_t kernel;         /* HEAT1D_KERNEL_*                                              */
+    int32_t blocking;       /* nonzero (default): heat1d_run returns after the device is done;
+                               zero: heat1d_run only enqueues on `stream`                   */
+    int32_t use_graphs;     /* nonzero (default): replay pass sequences as CUDA graphs      */
+    void *stream;           /* cudaStream_t for compute (e.g. torch's current stream);
+                               NULL = a stream owned by the handle                          */
+    void *comm_stream;      /* cudaStream_t for halo exchange; NULL = owned by the handle   */
+} heat1d_opts;
+
+/* Read-only facts about a handle (heat1d_info). */
+typedef struct {
+    uint32_t size;          /* = sizeof(heat1d_info_t)                                     */
+    int32_t T;              /* effective halo depth / steps per pass                        */
+    int32_t mode, denominator, kernel;
+    int32_t dp_ops;         /* fp64 instructions per cell update in the pass kernel (3 or 4) */
+    int32_t nslabs;         /* slabs held by this handle (virtual_slabs, else 1)            */
+    int32_t rank, nranks, device;
+    double r;               /* k*dt/D as used by the kernels                                */
+    int64_t N, first, count;/* ring size, this rank's slab [first, first+count)             */
+    int64_t steps_done;
+    int64_t launches;       /* kernels launched by this handle so far (all kinds)           */
+    int64_t pad;            /* ghost cells allocated on each side of a slab                 */
+    int32_t tile_cells;     /* output cells per CTA tile of the pass kernel (at T)          */
+    int32_t grid;           /* CTAs per pass-kernel launch (persistent)                     */
+} heat1d_info_t;
+
+/* Exchange plan of one rank (pure host logic; usable without a GPU).  Offsets
+ * are in cells relative to cell 0 of the rank's slab (negative = left pad). */
+typedef struct {
+    int32_t left, right;        /* neighbour ranks (g-1) mod G, (g+1) mod G                 */
+    int64_t send_right_off;     /* = count - T : last T cells, sent first  to `right`       */
+    int64_t send_left_off;      /* = 0         : first T cells, sent second to `left`       */
+    int64_t recv_left_off;      /* = -T        : left pad, received first  from `left`      */
+    int64_t recv_right_off;     /* = count     : right pad, received second from `right`    */
+    int64_t cells;              /* T cells per message (8T bytes)                           */
+} heat1d_exchange_plan;
+
+HEAT1D_API void heat1d_opts_default(heat1d_opts *o);
+HEAT1D_API int heat1d_version(void);
+HEAT1D_API const char *heat1d_strerror(int status);
+
+/* Slab of `rank` when N = nx*np cells are split over `nranks` contiguous slabs:
+ * partition-granular and front-loaded when np >= nranks, else
+ * cell-granular front-loaded.  Pure host function. */
+HEAT1D_API int heat1d_partition(int64_t nx, int64_t np, int32_t nranks, int32_t rank,
+                     int64_t *first, int64_t *count);
+
+/* Message plan of `rank` for one exchange of depth T (pure host function).
+ * Order matters when left == right (nranks == 2): NCCL and the reference CPU
+ * model issue send(right edge), send(left edge), recv(left pad), recv(right pad). */
+HEAT1D_API int heat1d_plan_exchange(int64_t nx, int64_t np, int32_t nranks, int32_t rank, int32_t T,
+                         heat1d_exchange_plan *plan);
+
+/* Doubles of device memory a handle with these arguments allocates. */
+HEAT1D_API int64_t heat1d_buffer_len(int64_t nx, int64_t np, const heat1d_opts *opts);
+
+/* rank 0 only: writes a 128-byte ncclUniqueId to out128 (host memory). */
+HEAT1D_API int heat1d_get_unique_id(void *out128);
+
+/* Validate, compute r, allocate 2 buffers of (count + 2*pad) fp64 per slab,
+ * create streams/events, and (nranks > 1) join the NCCL ring -- collective
+ * over all ranks.  nt is the default step count of heat1d_run(h, -1).
+ * Errors: EINVAL (nx<1, np<1, N>2^62, nt<0, k<0, dt<=0, dx<=0, non-finite,
+ * bad rank/nranks/T/virtual_slabs, count < T... see DESIGN.md §5), EUNSTABLE
+ * (r > 1/2), ENOMEM, ECUDA, ENCCL.  On error *out = NULL. */
+HEAT1D_API int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt,
+                  double k, double dt, double dx, const heat1d_opts *opts);
+
+/* This handle's slab [first, first+count) of the ring. */
+HEAT1D_API int heat1d_local_range(heat1d_t h, int64_t *first, int64_t *count);
+
+/* Copy u(0) of this rank's slab (count = local count, host or device pointer).
+ * The data is COPIED before return; the caller may free u0 at once.
+ * Resets steps_done to 0. */
+HEAT1D_API int heat1d_set_initial(heat1d_t h, const double *u0, int64_t count);
+
+/* Device-side initial condition u0[i] = lo + (hi-lo)*U(seed, i) for the global
+ * cell indices i of this slab, U = splitmix64 counter form (DESIGN.md §4,
+ * identical to synth.uniform).  Resets steps_done to 0. */
+HEAT1D_API int heat1d_init_uniform(heat1d_t h, uint64_t seed, double lo, double hi);
+
+/* Advance nt >= 0 steps (cumulative over calls; nt < 0 = create's nt).
+ * Collective over ranks when nranks > 1.  ESTATE before an initial state. */
+HEAT1D_API int heat1d_run(heat1d_t h, int64_t nt);
+
+/* Copy this slab's current state to out (host or device pointer), synchronous. */
+HEAT1D_API int heat1d_get(heat1d_t h, double *out, int64_t count);
+
+HEAT1D_API int64_t heat1d_steps_done(heat1d_t h);   /* -1 if h is NULL */
+HEAT1D_API int heat1d_info(heat1d_t h, heat1d_info_t *info);
+
+/* Per-launch timing of the dominant (pass) kernel with CUDA events on the
+ * compute stream.  heat1d_profile returns launches and summed milliseconds
+ * since profiling was enabled (synchronises the stream). */
+HEAT1D_API int heat1d_set_profiling(heat1d_t h, int on);
+HEAT1D_API int heat1d_profile(heat1d_t h, int64_t *launches, double *ms);
+
+/* Compute stream of the handle as a cudaStream_t (for the caller's events). */
+HEAT1D_API void *heat1d_stream(heat1d_t h);
+
+/* NULL-safe; frees library-owned memory, streams, events and the NCCL comm. */
+HEAT1D_API int heat1d_destroy(heat1d_t h);
+
+/* Message for the last failing call on h ("" if none). */
+HEAT1D_API const char *heat1d_last_error(heat1d_t h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEAT1D_H */

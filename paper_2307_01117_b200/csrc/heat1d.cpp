@@ -1,0 +1,688 @@
+// heat1d.cpp -- host runtime behind include/heat1d.h.
+//
+// One handle per rank.  A handle owns S slabs (S = virtual_slabs on one GPU,
+// else 1) of the periodic ring, each stored as two padded fp64 buffers
+//     [pad ghost cells | count cells | pad ghost cells]
+// (ping-pong, Jacobi: PAPER.md:68 reads time-t values only).
+// A "pass" advances T steps:
+//   single slab, single rank : K2 over [0,n) reading its own periodic pads,
+//                              which K2 rewrites for the next pass (self-halo)
+//   several slabs / ranks    : exchange depth-T halos with the ring neighbours
+//                              on the comm stream (NCCL send/recv, or device
+//                              copies between virtual slabs) while K2 updates
+//                              the interior [T, n-T); then K3 does the edges.
+// This is the paper's segmented ghost-zone algorithm with the
+// exchange done every T steps at depth T instead of every step at depth 1.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "heat1d.h"
+#include "kernels.h"
+
+using heat1d::PassGeom;
+
+namespace {
+
+struct Slab {
+    int64_t first = 0, count = 0;
+    double *buf[2] = {nullptr, nullptr};  // base of each padded buffer
+};
+
+thread_local std::string g_create_error;
+
+}  // namespace
+
+struct heat1d_s {
+    int device = 0;
+    int rank = 0, nranks = 1;
+    int64_t nx = 0, np = 0, N = 0, nt_default = 0;
+    double k = 0, dt = 0, dx = 0, r = 0;
+    int T = 8, mode = 0, den = 0, kernel = 0, ops = 4;
+    bool blocking = true, use_graphs = true;
+    int64_t pad = 16;
+    int64_t first = 0, count = 0;  // this rank's range (union of its slabs)
+    std::vector<Slab> slabs;
+    int cur = 0;
+    bool initialized = false;
+    int poisoned = 0;
+    int64_t steps_done = 0;
+    int64_t launches = 0;
+    int num_sms = 148;
+    PassGeom geom{17, 8, 3, 2};
+    int last_grid = 0;
+
+    cudaStream_t stream = nullptr, comm = nullptr;
+    bool own_stream = false, own_comm = false;
+    cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+    ncclComm_t nccl = nullptr;
+    void *alloc = nullptr;
+
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    int64_t prof_launches = 0;
+    double prof_ms = 0.0;
+
+    std::string last_error;
+
+    bool multi() const { return nranks > 1 || slabs.size() > 1; }
+};
+
+namespace {
+
+int set_error(heat1d_t h, int status, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (h)
+        h->last_error = buf;
+    else
+        g_create_error = buf;
+    return status;
+}
+
+int fail_cuda(heat1d_t h, cudaError_t e, const char *what, int line) {
+    if (h) h->poisoned = HEAT1D_ECUDA;
+    return set_error(h, HEAT1D_ECUDA, "CUDA error %s (%s) at heat1d.cpp:%d: %s", cudaGetErrorName(e),
+                     cudaGetErrorString(e), line, what);
+}
+
+int fail_nccl(heat1d_t h, ncclResult_t e, const char *what, int line) {
+    if (h) h->poisoned = HEAT1D_ENCCL;
+    return set_error(h, HEAT1D_ENCCL, "NCCL error %d (%s) at heat1d.cpp:%d: %s", (int)e, ncclGetErrorString(e),
+                     line, what);
+}
+
+#define CK(call)                                                     \
+    do {                                                             \
+        cudaError_t e_ = (call);                                     \
+        if (e_ != cudaSuccess) return fail_cuda(h, e_, #call, __LINE__); \
+    } while (0)
+
+#define NK(call)                                                     \
+    do {                                                             \
+        ncclResult_t e_ = (call);                                    \
+        if (e_ != ncclSuccess) return fail_nccl(h, e_, #call, __LINE__); \
+    } while (0)
+
+bool is_pow2(double r) {
+    if (!(r > 0.0) || !std::isfinite(r)) return false;
+    int e;
+    const double m = std::frexp(r, &e);
+    return m == 0.5 && r >= 2.2250738585072014e-308;  // normal power of two
+}
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+int64_t pad_for(int T) { return round_up((int64_t)T + 2, 16); }
+
+// Plain partition arithmetic (also exported as heat1d_partition).
+int partition(int64_t nx, int64_t np, int32_t G, int32_t g, int64_t *first, int64_t *count) {
+    if (nx < 1 || np < 1 || G < 1 || g < 0 || g >= G) return HEAT1D_EINVAL;
+    if (nx > ((int64_t)1 << 62) / np) return HEAT1D_EINVAL;
+    const int64_t N = nx * np;
+    if (np >= G) {  // whole partitions, front-loaded remainder
+        const int64_t base = np / G, rem = np % G;
+        const int64_t parts = base + (g < rem ? 1 : 0);
+        const int64_t p0 = (int64_t)g * base + (g < rem ? g : rem);
+        *first = p0 * nx;
+        *count = parts * nx;
+    } else {  // fewer partitions than slabs: split cells, front-loaded
+        if (N < G) return HEAT1D_EINVAL;
+        const int64_t base = N / G, rem = N % G;
+        *first = (int64_t)g * base + (g < rem ? g : rem);
+        *count = base + (g < rem ? 1 : 0);
+    }
+    return HEAT1D_OK;
+}
+
+int64_t min_slab(int64_t nx, int64_t np, int32_t G) {
+    int64_t mn = INT64_MAX, f, c;
+    for (int g = 0; g < G; ++g)
+        if (partition(nx, np, G, g, &f, &c) == HEAT1D_OK && c < mn) mn = c;
+    return mn;
+}
+
+int auto_T(int ops) {
+    // 4-op (matched, general r) is HBM-bound up to T~11 on B200;
+    // 3-op reaches the fp64 issue limit later.  Overridable via opts.T.
+    return ops == 4 ? 8 : 12;
+}
+
+bool parse_geom_env(PassGeom *g) {
+    const char *s = getenv("HEAT1D_GEOM");  // "V,NW,S,ctas_per_sm" (tuning knob)
+    if (!s || !*s) return false;
+    int v, nw, st, c;
+    if (sscanf(s, "%d,%d,%d,%d", &v, &nw, &st, &c) != 4) return false;
+    *g = PassGeom{v, nw, st, c};
+    return true;
+}
+
+cudaEvent_t prof_event(heat1d_t h) {
+    if (h->ev_used == h->ev_pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        h->ev_pool.push_back(e);
+    }
+    return h->ev_pool[h->ev_used++];
+}
+
+int prof_collect(heat1d_t h) {
+    if (h->ev_used == 0) return HEAT1D_OK;
+    CK(cudaStreamSynchronize(h->stream));
+    for (size_t i = 0; i + 1 < h->ev_used; i += 2) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev_pool[i], h->ev_pool[i + 1]));
+        h->prof_ms += ms;
+        h->prof_launches += 1;
+    }
+    h->ev_used = 0;
+    return HEAT1D_OK;
+}
+
+double *cell0(heat1d_t h, const Slab &s, int which) { return s.buf[which] + h->pad; }
+
+int launch_pass_slab(heat1d_t h, const Slab &s, int Tp, int64_t lo, int64_t hi, int wrapT) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->prof) {
+        e0 = prof_event(h);
+        e1 = prof_event(h);
+        if (!e0 || !e1) return set_error(h, HEAT1D_ECUDA, "event pool");
+        CK(cudaEventRecord(e0, h->stream));
+    }
+    int grid = 0;
+    CK(heat1d::launch_pass(h->geom, h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp, lo, hi,
+                           wrapT, h->r, h->num_sms, h->stream, &grid));
+    if (grid > 0) h->launches++;
+    h->last_grid = grid > 0 ? grid : h->last_grid;
+    if (h->prof) CK(cudaEventRecord(e1, h->stream));
+    return HEAT1D_OK;
+}
+
+// Fill the depth-Tp ghost pads of every slab of the current buffer from the
+// ring neighbours (comm stream).  Message plan = heat1d_plan_exchange.
+int exchange(heat1d_t h, int Tp) {
+    const int ns = (int)h->slabs.size();
+    const int cur = h->cur;
+    if (h->nranks > 1) {
+        const Slab &s = h->slabs[0];
+        double *A = cell0(h, s, cur);
+        const int left = (h->rank - 1 + h->nranks) % h->nranks;
+        const int right = (h->rank + 1) % h->nranks;
+        NK(ncclGroupStart());
+        NK(ncclSend(A + s.count - Tp, (size_t)Tp, ncclDouble, right, h->nccl, h->comm));
+        NK(ncclSend(A, (size_t)Tp, ncclDouble, left, h->nccl, h->comm));
+        NK(ncclRecv(A - Tp, (size_t)Tp, ncclDouble, left, h->nccl, h->comm));
+        NK(ncclRecv(A + s.count, (size_t)Tp, ncclDouble, right, h->nccl, h->comm));
+        NK(ncclGroupEnd());
+        return HEAT1D_OK;
+    }
+    // virtual slabs on one device: the same four messages as device copies
+    for (int g = 0; g < ns; ++g) {
+        const Slab &s = h->slabs[g];
+        const Slab &L = h->slabs[(g - 1 + ns) % ns];
+        const Slab &R = h->slabs[(g + 1) % ns];
+        double *A = cell0(h, s, cur);
+        CK(cudaMemcpyAsync(A - Tp, cell0(h, L, cur) + L.count - Tp, (size_t)Tp * 8, cudaMemcpyDeviceToDevice,
+                           h->comm));
+        CK(cudaMemcpyAsync(A + s.count, cell0(h, R, cur), (size_t)Tp * 8, cudaMemcpyDeviceToDevice, h->comm));
+    }
+    return HEAT1D_OK;
+}
+
+int run_passes(heat1d_t h, int64_t nt) {
+    int64_t done = 0;
+    while (done < nt) {
+        if (h->kernel == HEAT1D_KERNEL_NAIVE) {
+            const Slab &s = h->slabs[0];
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            if (h->prof) {
+                e0 = prof_event(h);
+                e1 = prof_event(h);
+                CK(cudaEventRecord(e0, h->stream));
+            }
+            CK(heat1d::launch_naive(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, h->r,
+                                    h->stream));
+            if (h->prof) CK(cudaEventRecord(e1, h->stream));
+            h->launches++;
+            h->cur ^= 1;
+            done += 1;
+            continue;
+        }
+        const int Tp = (int)((nt - done) < h->T ? (nt - done) : h->T);
+        if (!h->multi()) {
+            const Slab &s = h->slabs[0];
+            const int wrapT = (int)(h->T < s.count ? h->T : s.count);
+            int rc = launch_pass_slab(h, s, Tp, 0, s.count, wrapT);
+            if (rc) return rc;
+        } else {
+            CK(cudaEventRecord(h->ev_ready, h->stream));
+            CK(cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
+            int rc = exchange(h, Tp);
+            if (rc) return rc;
+            CK(cudaEventRecord(h->ev_halo, h->comm));
+            for (const Slab &s : h->slabs) {
+                rc = launch_pass_slab(h, s, Tp, Tp, s.count - Tp, 0);
+                if (rc) return rc;
+            }
+            CK(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+            for (const Slab &s : h->slabs) {
+                CK(heat1d::launch_edges(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp, h->r,
+                                        h->stream));
+                h->launches++;
+            }
+        }
+        h->cur ^= 1;
+        done += Tp;
+    }
+    h->steps_done += nt;
+    return HEAT1D_OK;
+}
+
+int guard(heat1d_t h) {
+    if (!h) return set_error(nullptr, HEAT1D_EINVAL, "NULL handle");
+    if (h->poisoned) return h->poisoned;
+    if (cudaSetDevice(h->device) != cudaSuccess) return set_error(h, HEAT1D_ECUDA, "cudaSetDevice failed");
+    return HEAT1D_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void heat1d_opts_default(heat1d_opts *o) {
+    if (!o) return;
+    memset(o, 0, sizeof *o);
+    o->size = sizeof *o;
+    o->device = -1;
+    o->rank = 0;
+    o->nranks = 1;
+    o->nccl_id = nullptr;
+    o->T = 0;
+    o->mode = HEAT1D_MODE_MATCHED;
+    o->denominator = HEAT1D_DEN_DX2;
+    o->allow_unstable = 0;
+    o->virtual_slabs = 1;
+    o->kernel = HEAT1D_KERNEL_AUTO;
+    o->blocking = 1;
+    o->use_graphs = 1;
+}
+
+int heat1d_version(void) { return HEAT1D_VERSION; }
+
+const char *heat1d_strerror(int status) {
+    switch (status) {
+        case HEAT1D_OK: return "ok";
+        case HEAT1D_EINVAL: return "invalid argument";
+        case HEAT1D_EUNSTABLE: return "unstable: r = k*dt/D > 1/2 (set allow_unstable)";
+        case HEAT1D_ESTATE: return "invalid state (no initial condition, or poisoned handle)";
+        case HEAT1D_ENOMEM: return "out of device memory";
+        case HEAT1D_ECUDA: return "CUDA error";
+        case HEAT1D_ENCCL: return "NCCL error";
+        case HEAT1D_EUNSUPPORTED: return "unsupported";
+        default: return "unknown status";
+    }
+}
+
+int heat1d_partition(int64_t nx, int64_t np, int32_t nranks, int32_t rank, int64_t *first, int64_t *count) {
+    if (!first || !count) return HEAT1D_EINVAL;
+    return partition(nx, np, nranks, rank, first, count);
+}
+
+int heat1d_plan_exchange(int64_t nx, int64_t np, int32_t nranks, int32_t rank, int32_t T,
+                         heat1d_exchange_plan *plan) {
+    if (!plan || T < 1) return HEAT1D_EINVAL;
+    int64_t first, count;
+    int rc = partition(nx, np, nranks, rank, &first, &count);
+    if (rc) return rc;
+    if (T > min_slab(nx, np, nranks)) return HEAT1D_EINVAL;
+    plan->left = (rank - 1 + nranks) % nranks;
+    plan->right = (rank + 1) % nranks;
+    plan->send_right_off = count - T;
+    plan->send_left_off = 0;
+    plan->recv_left_off = -(int64_t)T;
+    plan->recv_right_off = count;
+    plan->cells = T;
+    return HEAT1D_OK;
+}
+
+int64_t heat1d_buffer_len(int64_t nx, int64_t np, const heat1d_opts *o) {
+    heat1d_opts d;
+    if (!o) {
+        heat1d_opts_default(&d);
+        o = &d;
+    }
+    const int G = o->virtual_slabs > 1 ? o->virtual_slabs : o->nranks;
+    const int rank = o->virtual_slabs > 1 ? -1 : o->rank;
+    const int T = o->T > 0 ? o->T : 12;
+    const int64_t pad = pad_for(T);
+    int64_t total = 0, f, c;
+    for (int g = 0; g < G; ++g) {
+        if (rank >= 0 && g != rank) continue;
+        if (partition(nx, np, G, g, &f, &c) != HEAT1D_OK) return -1;
+        total += 2 * round_up(c + 2 * pad, 32);
+    }
+    return total;
+}
+
+int heat1d_get_unique_id(void *out128) {
+    if (!out128) return HEAT1D_EINVAL;
+    ncclUniqueId id;
+    ncclResult_t e = ncclGetUniqueId(&id);
+    if (e != ncclSuccess) return set_error(nullptr, HEAT1D_ENCCL, "ncclGetUniqueId: %s", ncclGetErrorString(e));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    memcpy(out128, &id, sizeof id);
+    return HEAT1D_OK;
+}
+
+int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, double dt, double dx,
+                  const heat1d_opts *opts) {
+    if (!out) return set_error(nullptr, HEAT1D_EINVAL, "out is NULL");
+    *out = nullptr;
+    heat1d_opts o;
+    heat1d_opts_default(&o);
+    if (opts) {
+        if (opts->size != sizeof(heat1d_opts))
+            return set_error(nullptr, HEAT1D_EINVAL, "opts.size %u != %zu", opts->size, sizeof(heat1d_opts));
+        o = *opts;
+    }
+    if (nx < 1 || np < 1) return set_error(nullptr, HEAT1D_EINVAL, "nx and np must be >= 1");
+    if (nx > ((int64_t)1 << 62) / np) return set_error(nullptr, HEAT1D_EINVAL, "nx*np exceeds 2^62");
+    if (nt < 0) return set_error(nullptr, HEAT1D_EINVAL, "nt must be >= 0");
+    if (!std::isfinite(k) || !std::isfinite(dt) || !std::isfinite(dx))
+        return set_error(nullptr, HEAT1D_EINVAL, "k, dt, dx must be finite");
+    if (k < 0 || dt <= 0 || dx <= 0) return set_error(nullptr, HEAT1D_EINVAL, "need k >= 0, dt > 0, dx > 0");
+    if (o.mode != HEAT1D_MODE_MATCHED && o.mode != HEAT1D_MODE_FAST)
+        return set_error(nullptr, HEAT1D_EINVAL, "bad mode");
+    if (o.denominator != HEAT1D_DEN_DX2 && o.denominator != HEAT1D_DEN_PAPER_2DX)
+        return set_error(nullptr, HEAT1D_EINVAL, "bad denominator");
+    if (o.kernel != HEAT1D_KERNEL_AUTO && o.kernel != HEAT1D_KERNEL_NAIVE)
+        return set_error(nullptr, HEAT1D_EINVAL, "bad kernel");
+    if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks)
+        return set_error(nullptr, HEAT1D_EINVAL, "bad rank %d / nranks %d", o.rank, o.nranks);
+    if (o.nranks > 1 && !o.nccl_id) return set_error(nullptr, HEAT1D_EINVAL, "nranks > 1 needs nccl_id");
+    if (o.virtual_slabs < 1) return set_error(nullptr, HEAT1D_EINVAL, "virtual_slabs must be >= 1");
+    if (o.virtual_slabs > 1 && o.nranks > 1)
+        return set_error(nullptr, HEAT1D_EUNSUPPORTED, "virtual_slabs > 1 needs nranks == 1");
+    if (o.T < 0 || o.T > HEAT1D_T_MAX) return set_error(nullptr, HEAT1D_EINVAL, "T must be in 0..%d", HEAT1D_T_MAX);
+    const int G = o.virtual_slabs > 1 ? o.virtual_slabs : o.nranks;
+    if (o.kernel == HEAT1D_KERNEL_NAIVE && G > 1)
+        return set_error(nullptr, HEAT1D_EUNSUPPORTED, "the naive kernel is single-slab only");
+
+    // r once on the host, fp64 (reading c4)
+    const double r = (o.denominator == HEAT1D_DEN_DX2) ? (k * dt) / (dx * dx) : (k * dt) / (2.0 * dx);
+    if (!std::isfinite(r)) return set_error(nullptr, HEAT1D_EINVAL, "r is not finite");
+    if (r > 0.5 && !o.allow_unstable)
+        return set_error(nullptr, HEAT1D_EUNSTABLE, "r = %.17g > 1/2 (CFL); set allow_unstable", r);
+
+    const int64_t mslab = min_slab(nx, np, G);
+    if (mslab == INT64_MAX) return set_error(nullptr, HEAT1D_EINVAL, "cannot split N=%lld into %d slabs",
+                                             (long long)(nx * np), G);
+
+    heat1d_t h = new heat1d_s();
+    h->nx = nx;
+    h->np = np;
+    h->N = nx * np;
+    h->nt_default = nt;
+    h->k = k;
+    h->dt = dt;
+    h->dx = dx;
+    h->r = r;
+    h->mode = o.mode;
+    h->den = o.denominator;
+    h->kernel = o.kernel;
+    h->rank = o.rank;
+    h->nranks = o.nranks;
+    h->blocking = o.blocking != 0;
+    h->use_graphs = o.use_graphs != 0;
+    h->ops = (o.mode == HEAT1D_MODE_FAST || is_pow2(r) || r == 0.0) ? 3 : 4;
+    // r == 0: fma(0, t, b) == b + 0*t == b for finite t (identity either way)
+    int T = o.T > 0 ? o.T : auto_T(h->ops);
+    if (o.kernel == HEAT1D_KERNEL_NAIVE) T = 1;
+    if (T > mslab) T = (int)mslab;  // a slab must hold its own halo
+    h->T = T;
+    h->pad = pad_for(T);
+
+    auto bail = [&](int rc) {
+        heat1d_destroy(h);
+        return rc;
+    };
+
+    if (o.device >= 0) {
+        cudaError_t e = cudaSetDevice(o.device);
+        if (e != cudaSuccess) {
+            set_error(nullptr, HEAT1D_ECUDA, "cudaSetDevice(%d): %s", o.device, cudaGetErrorString(e));
+            delete h;
+            return HEAT1D_ECUDA;
+        }
+    }
+    if (cudaGetDevice(&h->device) != cudaSuccess) {
+        delete h;
+        return set_error(nullptr, HEAT1D_ECUDA, "no CUDA device");
+    }
+    cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
+
+    // slabs
+    const int ns = o.virtual_slabs;
+    int64_t total = 0;
+    for (int g = 0; g < ns; ++g) {
+        Slab s;
+        const int idx = (ns > 1) ? g : o.rank;
+        partition(nx, np, G, idx, &s.first, &s.count);
+        h->slabs.push_back(s);
+        total += 2 * round_up(s.count + 2 * h->pad, 32);
+    }
+    h->first = h->slabs.front().first;
+    h->count = 0;
+    for (auto &s : h->slabs) h->count += s.count;
+
+    cudaError_t e = cudaMalloc(&h->alloc, (size_t)total * sizeof(double));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error(nullptr, HEAT1D_ENOMEM, "cudaMalloc(%lld bytes): %s", (long long)total * 8, cudaGetErrorString(e));
+        return bail(HEAT1D_ENOMEM);
+    }
+    double *p = static_cast<double *>(h->alloc);
+    for (auto &s : h->slabs) {
+        const int64_t len = round_up(s.count + 2 * h->pad, 32);
+        s.buf[0] = p;
+        s.buf[1] = p + len;
+        p += 2 * len;
+    }
+
+    if (o.stream) {
+        h->stream = static_cast<cudaStream_t>(o.stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            set_error(nullptr, HEAT1D_ECUDA, "stream create");
+            return bail(HEAT1D_ECUDA);
+        }
+        h->own_stream = true;
+    }
+    if (G > 1) {
+        if (o.comm_stream) {
+            h->comm = static_cast<cudaStream_t>(o.comm_stream);
+        } else {
+            if (cudaStreamCreateWithFlags(&h->comm, cudaStreamNonBlocking) != cudaSuccess) {
+                set_error(nullptr, HEAT1D_ECUDA, "stream create");
+                return bail(HEAT1D_ECUDA);
+            }
+            h->own_comm = true;
+        }
+        if (cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming) != cudaSuccess) {
+            set_error(nullptr, HEAT1D_ECUDA, "event create");
+            return bail(HEAT1D_ECUDA);
+        }
+    }
+    if (o.nranks > 1) {
+        ncclUniqueId id;
+        memcpy(&id, o.nccl_id, sizeof id);
+        ncclResult_t ne = ncclCommInitRank(&h->nccl, o.nranks, id, o.rank);
+        if (ne != ncclSuccess) {
+            h->nccl = nullptr;
+            set_error(nullptr, HEAT1D_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(ne));
+            return bail(HEAT1D_ENCCL);
+        }
+    }
+    if (!parse_geom_env(&h->geom)) h->geom = heat1d::choose_geom(h->slabs[0].count, h->T, h->num_sms);
+    *out = h;
+    return HEAT1D_OK;
+}
+
+int heat1d_local_range(heat1d_t h, int64_t *first, int64_t *count) {
+    if (!h || !first || !count) return HEAT1D_EINVAL;
+    *first = h->first;
+    *count = h->count;
+    return HEAT1D_OK;
+}
+
+static int after_initial(heat1d_t h) {
+    if (!h->multi()) {
+        const Slab &s = h->slabs[0];
+        CK(heat1d::launch_wrap_fill(cell0(h, s, h->cur), s.count, h->pad, h->stream));
+        h->launches++;
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    h->initialized = true;
+    h->steps_done = 0;
+    return HEAT1D_OK;
+}
+
+int heat1d_set_initial(heat1d_t h, const double *u0, int64_t count) {
+    int rc = guard(h);
+    if (rc) return rc;
+    if (!u0) return set_error(h, HEAT1D_EINVAL, "u0 is NULL");
+    if (count != h->count)
+        return set_error(h, HEAT1D_EINVAL, "count %lld != local slab %lld", (long long)count, (long long)h->count);
+    int64_t off = 0;
+    for (const Slab &s : h->slabs) {
+        CK(cudaMemcpyAsync(cell0(h, s, h->cur), u0 + off, (size_t)s.count * 8, cudaMemcpyDefault, h->stream));
+        off += s.count;
+    }
+    return after_initial(h);
+}
+
+int heat1d_init_uniform(heat1d_t h, uint64_t seed, double lo, double hi) {
+    int rc = guard(h);
+    if (rc) return rc;
+    if (!std::isfinite(lo) || !std::isfinite(hi)) return set_error(h, HEAT1D_EINVAL, "lo/hi not finite");
+    for (const Slab &s : h->slabs) {
+        CK(heat1d::launch_init_uniform(cell0(h, s, h->cur), s.count, s.first, seed, lo, hi, h->stream));
+        h->launches++;
+    }
+    return after_initial(h);
+}
+
+int heat1d_run(heat1d_t h, int64_t nt) {
+    int rc = guard(h);
+    if (rc) return rc;
+    if (!h->initialized) return set_error(h, HEAT1D_ESTATE, "run before set_initial");
+    if (nt < 0) nt = h->nt_default;
+    if (nt == 0) return HEAT1D_OK;
+    rc = run_passes(h, nt);
+    if (rc) return rc;
+    if (h->blocking) {
+        CK(cudaStreamSynchronize(h->stream));
+        if (h->prof) {
+            rc = prof_collect(h);
+            if (rc) return rc;
+        }
+    }
+    return HEAT1D_OK;
+}
+
+int heat1d_get(heat1d_t h, double *out, int64_t count) {
+    int rc = guard(h);
+    if (rc) return rc;
+    if (!out) return set_error(h, HEAT1D_EINVAL, "out is NULL");
+    if (!h->initialized) return set_error(h, HEAT1D_ESTATE, "get before set_initial");
+    if (count != h->count)
+        return set_error(h, HEAT1D_EINVAL, "count %lld != local slab %lld", (long long)count, (long long)h->count);
+    int64_t off = 0;
+    for (const Slab &s : h->slabs) {
+        CK(cudaMemcpyAsync(out + off, cell0(h, s, h->cur), (size_t)s.count * 8, cudaMemcpyDefault, h->stream));
+        off += s.count;
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    return HEAT1D_OK;
+}
+
+int64_t heat1d_steps_done(heat1d_t h) { return h ? h->steps_done : -1; }
+
+int heat1d_info(heat1d_t h, heat1d_info_t *info) {
+    if (!h || !info) return HEAT1D_EINVAL;
+    if (info->size != sizeof(heat1d_info_t)) return HEAT1D_EINVAL;
+    info->T = h->T;
+    info->mode = h->mode;
+    info->denominator = h->den;
+    info->kernel = h->kernel;
+    info->dp_ops = h->ops;
+    info->nslabs = (int32_t)h->slabs.size();
+    info->rank = h->rank;
+    info->nranks = h->nranks;
+    info->device = h->device;
+    info->r = h->r;
+    info->N = h->N;
+    info->first = h->first;
+    info->count = h->count;
+    info->steps_done = h->steps_done;
+    info->launches = h->launches;
+    info->pad = h->pad;
+    info->tile_cells = (int32_t)h->geom.tile_out(h->T);
+    info->grid = h->last_grid;
+    return HEAT1D_OK;
+}
+
+int heat1d_set_profiling(heat1d_t h, int on) {
+    int rc = guard(h);
+    if (rc) return rc;
+    rc = prof_collect(h);
+    if (rc) return rc;
+    h->prof = on != 0;
+    h->prof_ms = 0.0;
+    h->prof_launches = 0;
+    return HEAT1D_OK;
+}
+
+int heat1d_profile(heat1d_t h, int64_t *launches, double *ms) {
+    int rc = guard(h);
+    if (rc) return rc;
+    rc = prof_collect(h);
+    if (rc) return rc;
+    if (launches) *launches = h->prof_launches;
+    if (ms) *ms = h->prof_ms;
+    return HEAT1D_OK;
+}
+
+void *heat1d_stream(heat1d_t h) { return h ? (void *)h->stream : nullptr; }
+
+int heat1d_destroy(heat1d_t h) {
+    if (!h) return HEAT1D_OK;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->comm) cudaStreamSynchronize(h->comm);
+    if (h->nccl) ncclCommDestroy(h->nccl);
+    for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+    if (h->ev_ready) cudaEventDestroy(h->ev_ready);
+    if (h->ev_halo) cudaEventDestroy(h->ev_halo);
+    if (h->own_comm && h->comm) cudaStreamDestroy(h->comm);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    if (h->alloc) cudaFree(h->alloc);
+    delete h;
+    return HEAT1D_OK;
+}
+
+const char *heat1d_last_error(heat1d_t h) { return h ? h->last_error.c_str() : g_create_error.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,394 @@
+// kernels.cu -- sm_100a kernels of libheat1d.
+//
+//   K2 k2_pass      T fused Jacobi steps of Eq. 2 per HBM pass (the hot kernel)
+//   K1 k1_naive     one step per launch, modular indexing (T = 1 baseline)
+//   K3 k3_edges     the two T-wide edge strips of a slab once its ghosts arrived
+//   K4 k4_wrap_fill periodic self-halo of a single-slab ring
+//   K0 k0_uniform   splitmix64 initial condition (same counter generator as synth/)
+//
+// Eq. 2 on the periodic ring, segmented with
+// ghost zones.  The arithmetic is stencil.cuh; DESIGN.md §6
+// describes the data layout and the roofline of each kernel.
+#include <cstdio>
+#include <cstdint>
+#include <mutex>
+
+#include "kernels.h"
+#include "stencil.cuh"
+
+namespace heat1d {
+
+// ------------------------------------------------------------------ PTX helpers
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+
+// TMA 1D bulk copy global -> shared, completion counted on an mbarrier (SASS: UBLKCP).
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+// TMA 1D bulk copy shared -> global, tracked by bulk async-groups.
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Order this thread's generic-proxy shared-memory accesses before later async-proxy (TMA) ones.
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+constexpr unsigned FULL = 0xffffffffu;
+
+}  // namespace
+
+// ------------------------------------------------------------------ K2
+//
+// Persistent CTAs walk output tiles of W = NW*(32V - 2T) cells, round robin.
+// Tile [x0, x1) needs inputs [x0-T, x1+T): one TMA bulk copy (aligned down/up
+// to 16 B) lands them in an S-stage shared-memory ring (mbarrier complete_tx).
+// Warp w takes the 32V-cell span starting at w*(32V-2T) of the tile input;
+// lane l holds V consecutive cells in registers.  Each of the T steps fetches
+// the two inter-lane neighbours with shuffles; the warp's outermost cells go
+// stale by one cell per step (a per-warp trapezoid), so after T steps the
+// warp's 32V-2T central cells are exact.  Those are written back in place,
+// and one bulk copy stores the tile.  V odd makes the 64-bit shared accesses
+// of a half-warp hit 16 distinct bank pairs.
+template <int V, int NW, int S, int OPS>
+__global__ void __launch_bounds__(NW * 32)
+k2_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t out_lo,
+        int64_t out_hi, int wrapT, double r, int64_t ntiles, uint32_t stage_doubles) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);
+    double *stages = reinterpret_cast<double *>(smem_raw + 128);
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int OW = 32 * V - 2 * T;
+    const int64_t W = (int64_t)NW * OW;
+
+    const uint64_t pol_in = policy_evict_first();
+
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const int64_t stride = gridDim.x;
+
+    auto issue_load = [&](int64_t tile, int s) {
+        const int64_t x0 = out_lo + tile * W;
+        const int64_t x1 = min(x0 + W, out_hi);
+        const int64_t lo = x0 - T;
+        const int64_t ld_lo = lo - (lo & 1);
+        int64_t ld_hi = x1 + T;
+        ld_hi += (ld_hi & 1);
+        const uint32_t bytes = (uint32_t)((ld_hi - ld_lo) * 8);
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_g2s(stages + (size_t)s * stage_doubles, A + ld_lo, bytes, &full[s], pol_in);
+    };
+
+    if (tid == 0) {
+        for (int i = 0; i < S - 1; ++i) {
+            const int64_t tile = blockIdx.x + i * stride;
+            if (tile >= ntiles) break;
+            issue_load(tile, i);
+        }
+    }
+
+    int k = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += stride, ++k) {
+        const int s = k % S;
+        const uint32_t parity = (uint32_t)((k / S) & 1);
+        double *st = stages + (size_t)s * stage_doubles;
+
+        const int64_t x0 = out_lo + tile * W;
+        const int64_t x1 = min(x0 + W, out_hi);
+        const int64_t lo = x0 - T;
+        const int sh = (int)(lo & 1);
+        const int64_t ld_lo = lo - sh;
+
+        mbar_wait(&full[s], parity);
+
+        const int base = sh + warp * OW + lane * V;
+        double u[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) u[j] = st[base + j];
+
+        __syncthreads();  // B1: every warp has its span in registers -> in-place writes are safe
+
+        for (int step = 0; step < T; ++step) {
+            const double L = __shfl_up_sync(FULL, u[V - 1], 1);
+            const double R = __shfl_down_sync(FULL, u[0], 1);
+            double prev = L;
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                const double b = u[j];
+                const double c = (j + 1 < V) ? u[j + 1] : R;
+                u[j] = eq2<OPS>(prev, b, c, r);
+                prev = b;
+            }
+        }
+
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const int p = lane * V + j;
+            if (p >= T && p < 32 * V - T) st[base + j] = u[j];
+        }
+        fence_proxy_async();
+        __syncthreads();  // B2: tile outputs complete in shared memory
+
+        if (tid == 0) {
+            const int64_t a = x0 + (x0 & 1);
+            const int64_t b = x1 - (x1 & 1);
+            if (b > a) bulk_s2g(B + a, st + (a - ld_lo), (uint32_t)((b - a) * 8));
+            bulk_commit();  // one group per tile, possibly empty
+            const int64_t nxt = tile + (int64_t)(S - 1) * stride;
+            if (nxt < ntiles) {
+                bulk_wait_read<1>();  // the store that last used stage (k+S-1)%S has read it
+                fence_proxy_async();
+                issue_load(nxt, (k + S - 1) % S);
+            }
+            if (x0 & 1) B[x0] = st[x0 - ld_lo];
+        }
+        if (tid == 1 && (x1 & 1) && x1 - 1 >= x0) B[x1 - 1] = st[x1 - 1 - ld_lo];
+        for (int j = tid; j < wrapT; j += blockDim.x) {
+            if (j >= x0 && j < x1) B[n + j] = st[j - ld_lo];
+            const int64_t c = n - wrapT + j;
+            if (c >= x0 && c < x1) B[j - wrapT] = st[c - ld_lo];
+        }
+    }
+    if (tid == 0) bulk_wait<0>();
+}
+
+size_t PassGeom::smem_bytes(int T) const {
+    const int64_t in_cells = tile_out(T) + 2 * T + 2;
+    const int64_t stage = (in_cells + 15) / 16 * 16;
+    return 128 + (size_t)S * (size_t)stage * sizeof(double);
+}
+
+namespace {
+
+using PassFn = void (*)(const double *, double *, int64_t, int, int64_t, int64_t, int, double, int64_t,
+                        uint32_t);
+
+template <int V, int NW, int S, int OPS>
+PassFn pass_fn() {
+    return &k2_pass<V, NW, S, OPS>;
+}
+
+#define HEAT1D_GEOMS(X)                                                                            \
+    X(9, 4, 3) X(9, 4, 4) X(9, 8, 3) X(9, 8, 4) X(17, 4, 3) X(17, 4, 4) X(17, 8, 2) X(17, 8, 3)  \
+    X(17, 8, 4) X(25, 4, 3) X(25, 4, 4) X(25, 8, 3) X(25, 8, 4) X(33, 4, 3) X(33, 8, 3)
+
+PassFn lookup_pass(int V, int NW, int S, int ops) {
+#define X(v, nw, s)                                                                                \
+    if (V == v && NW == nw && S == s) return ops == 4 ? pass_fn<v, nw, s, 4>() : pass_fn<v, nw, s, 3>();
+    HEAT1D_GEOMS(X)
+#undef X
+    return nullptr;
+}
+
+}  // namespace
+
+PassGeom choose_geom(int64_t n_out, int T, int num_sms) {
+    // Default: V=17 (odd), 8 compute warps, 3 stages, 2 CTAs per SM (16 warps/SM,
+    // ~2 x 104 KB of the 228 KB shared memory).  Small rings get smaller tiles so
+    // that every SM has work.
+    PassGeom g{17, 8, 3, 2};
+    const int64_t want_tiles = (int64_t)num_sms * g.ctas_per_sm;
+    if (n_out < want_tiles * g.tile_out(T)) g = PassGeom{9, 4, 4, 4};
+    return g;
+}
+
+cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, int64_t n, int T,
+                        int64_t out_lo, int64_t out_hi, int wrapT, double r, int num_sms,
+                        cudaStream_t st, int *grid_out) {
+    PassFn fn = lookup_pass(g.V, g.NW, g.S, ops);
+    if (!fn) return cudaErrorInvalidConfiguration;
+    if (out_hi <= out_lo) {
+        if (grid_out) *grid_out = 0;
+        return cudaSuccess;
+    }
+    const int64_t W = g.tile_out(T);
+    if (W <= 0) return cudaErrorInvalidValue;
+    const int64_t ntiles = (out_hi - out_lo + W - 1) / W;
+    const size_t smem = g.smem_bytes(T);
+    const int64_t in_cells = W + 2 * T + 2;
+    const uint32_t stage_doubles = (uint32_t)((in_cells + 15) / 16 * 16);
+    // Raise the dynamic shared-memory limit once per instantiation (max over T).
+    {
+        static std::mutex mu;
+        static size_t done_bytes[64] = {0};
+        static PassFn done_fn[64] = {nullptr};
+        std::lock_guard<std::mutex> lk(mu);
+        int slot = -1;
+        for (int i = 0; i < 64; ++i) {
+            if (done_fn[i] == fn) { slot = i; break; }
+            if (done_fn[i] == nullptr) { slot = i; break; }
+        }
+        if (slot >= 0 && (done_fn[slot] != fn || done_bytes[slot] < smem)) {
+            const size_t want = g.smem_bytes(1);  // the largest tile (T=1)
+            cudaError_t e = cudaFuncSetAttribute((const void *)fn,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+            if (e != cudaSuccess) return e;
+            done_fn[slot] = fn;
+            done_bytes[slot] = want;
+        }
+    }
+    int64_t grid = (int64_t)num_sms * g.ctas_per_sm;
+    if (grid > ntiles) grid = ntiles;
+    if (grid_out) *grid_out = (int)grid;
+    fn<<<(unsigned)grid, g.NW * 32, smem, st>>>(A, B, n, T, out_lo, out_hi, wrapT, r, ntiles, stage_doubles);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K1
+template <int OPS>
+__global__ void __launch_bounds__(256) k1_naive(const double *__restrict__ A, double *__restrict__ B, int64_t n,
+                                                double r) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int64_t il = (i == 0) ? n - 1 : i - 1;  // periodic
+        const int64_t ir = (i == n - 1) ? 0 : i + 1;
+        B[i] = eq2<OPS>(A[il], A[i], A[ir], r);
+    }
+}
+
+cudaError_t launch_naive(int ops, const double *A, double *B, int64_t n, double r, cudaStream_t st) {
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (ops == 4)
+        k1_naive<4><<<(unsigned)blocks, 256, 0, st>>>(A, B, n, r);
+    else
+        k1_naive<3><<<(unsigned)blocks, 256, 0, st>>>(A, B, n, r);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K3
+// Block 0: outputs [0,T) from A[-T, 2T); block 1: outputs [n-T, n) from A[n-2T, n+T).
+// The 3T-cell window shrinks by one cell per side per step (light cone).
+template <int OPS>
+__global__ void __launch_bounds__(96) k3_edges(const double *__restrict__ A, double *__restrict__ B, int64_t n,
+                                               int T, double r) {
+    __shared__ double w[2][3 * 32];
+    const int64_t base = (blockIdx.x == 0) ? -(int64_t)T : n - 2 * (int64_t)T;
+    const int len = 3 * T;
+    for (int i = threadIdx.x; i < len; i += blockDim.x) w[0][i] = A[base + i];
+    __syncthreads();
+    int cur = 0;
+    for (int s = 0; s < T; ++s) {
+        const int lo = s + 1, hi = len - 1 - s;  // cells valid after step s+1
+        for (int i = lo + threadIdx.x; i < hi; i += blockDim.x)
+            w[cur ^ 1][i] = eq2<OPS>(w[cur][i - 1], w[cur][i], w[cur][i + 1], r);
+        cur ^= 1;
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < T; i += blockDim.x) B[base + T + i] = w[cur][T + i];
+}
+
+cudaError_t launch_edges(int ops, const double *A, double *B, int64_t n, int T, double r, cudaStream_t st) {
+    if (T < 1 || T > 32) return cudaErrorInvalidValue;
+    if (ops == 4)
+        k3_edges<4><<<2, 96, 0, st>>>(A, B, n, T, r);
+    else
+        k3_edges<3><<<2, 96, 0, st>>>(A, B, n, T, r);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K4
+__global__ void k4_wrap_fill(double *A, int64_t n, int64_t pad) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < pad; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = j % n;
+        A[n + j] = A[m];           // right pad: cells 0, 1, ...
+        A[-1 - j] = A[n - 1 - m];  // left pad:  cells n-1, n-2, ...
+    }
+}
+
+cudaError_t launch_wrap_fill(double *A, int64_t n, int64_t pad, cudaStream_t st) {
+    k4_wrap_fill<<<1, 128, 0, st>>>(A, n, pad);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K0
+__global__ void k0_uniform(double *u, int64_t count, int64_t first, uint64_t seed, double lo, double hi) {
+    const double d = __dsub_rn(hi, lo);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        uint64_t z = seed + (uint64_t)(first + i + 1) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const double U = __dmul_rn((double)(z >> 11), 0x1.0p-53);
+        u[i] = __dadd_rn(lo, __dmul_rn(d, U));
+    }
+}
+
+cudaError_t launch_init_uniform(double *u, int64_t count, int64_t first, uint64_t seed, double lo, double hi,
+                                cudaStream_t st) {
+    if (count <= 0) return cudaSuccess;
+    int64_t blocks = (count + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    k0_uniform<<<(unsigned)blocks, 256, 0, st>>>(u, count, first, seed, lo, hi);
+    return cudaGetLastError();
+}
+
+}  // namespace heat1d

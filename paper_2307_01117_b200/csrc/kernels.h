@@ -1,0 +1,48 @@
+// kernels.h -- internal launcher interface between the runtime (heat1d.cpp)
+// and the sm_100a kernels (kernels.cu).  Not part of the public C ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace heat1d {
+
+// Arithmetic variants of Eq. 2 (see stencil.cuh).
+enum Ops { OPS_MATCHED4 = 4, OPS_FMA3 = 3 };
+
+// Geometry of the temporal-blocked pass kernel (K2) for one launch config.
+struct PassGeom {
+    int V;            // cells per thread (odd: conflict-free 64-bit LDS/STS)
+    int NW;           // compute warps per CTA
+    int S;            // TMA pipeline stages
+    int ctas_per_sm;  // resident CTAs per SM the config is sized for
+    size_t smem_bytes(int T) const;
+    int64_t tile_out(int T) const { return (int64_t)NW * (32 * V - 2 * T); }
+};
+
+// Pick the pass-kernel configuration for (n, T).
+PassGeom choose_geom(int64_t n_out, int T, int num_sms);
+
+// K2: T fused Jacobi steps over outputs [out_lo, out_hi) of a slab.
+// A, B point at cell 0 of padded slab buffers (ghost cells at negative
+// offsets and at [n, n+pad)).  Reads A[out_lo-T, out_hi+T), writes B[out_lo, out_hi).
+// wrapT > 0 (single-slab ring): cells [0,wrapT) are also written to
+// B[n, n+wrapT) and cells [n-wrapT, n) to B[-wrapT, 0)  (periodic self-halo).
+cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, int64_t n,
+                        int T, int64_t out_lo, int64_t out_hi, int wrapT, double r,
+                        int num_sms, cudaStream_t st, int *grid_out);
+
+// K1: one step over the whole ring with modular indexing (no pads used).
+cudaError_t launch_naive(int ops, const double *A, double *B, int64_t n, double r, cudaStream_t st);
+
+// K3: the two edge strips [0,T) and [n-T,n) of a slab after its ghosts arrived.
+cudaError_t launch_edges(int ops, const double *A, double *B, int64_t n, int T, double r,
+                         cudaStream_t st);
+
+// K4: fill `pad` ghost cells on each side of a single-slab ring, modularly.
+cudaError_t launch_wrap_fill(double *A, int64_t n, int64_t pad, cudaStream_t st);
+
+// K0: u[i] = lo + (hi-lo) * U(seed, first+i), splitmix64 counter form.
+cudaError_t launch_init_uniform(double *u, int64_t count, int64_t first, uint64_t seed,
+                                double lo, double hi, cudaStream_t st);
+
+}  // namespace heat1d

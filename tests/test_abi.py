@@ -1,0 +1,164 @@
+"""C-ABI boundary checks that need no GPU (-m "not gpu"):
+the library builds/loads, exports every symbol include/heat1d.h declares,
+struct layouts match the header, argument validation happens before any CUDA
+call, and the pure host logic (partition, exchange plan) is right."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import subprocess
+import textwrap
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "heat1d.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2307_01117_b200 import _build
+    _build.build()
+    import paper_2307_01117_b200 as h1
+    return h1.load()
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"HEAT1D_API[^;]*?\b(heat1d_\w+)\s*\(", src, flags=re.S)))
+
+
+def test_exports_every_declared_symbol(lib):
+    import paper_2307_01117_b200 as h1
+    decl = declared_symbols()
+    assert len(decl) >= 20
+    out = subprocess.check_output(["nm", "-D", "--defined-only", os.path.join(ROOT, "paper_2307_01117_b200",
+                                                                             "libheat1d.so")], text=True)
+    exported = set(re.findall(r"\bT (heat1d_\w+)", out))
+    missing = [s for s in decl if s not in exported]
+    assert not missing, missing
+    assert sorted(h1.EXPORTS) == decl
+    for s in decl:
+        assert hasattr(lib, s)
+
+
+def test_no_oracle_in_product():
+    """The product library and binding never reference the oracle."""
+    pkg = os.path.join(ROOT, "paper_2307_01117_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cpp", ".h", ".cuh")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "oracle_run" not in txt, f
+    out = subprocess.check_output(["nm", "-D", os.path.join(pkg, "libheat1d.so")], text=True)
+    assert "oracle" not in out
+
+
+def test_struct_layout_matches_header(lib, tmp_path):
+    import paper_2307_01117_b200.heat1d as b
+    prog = tmp_path / "sz.c"
+    prog.write_text(textwrap.dedent("""
+        #include <stdio.h>
+        #include <stddef.h>
+        #include "heat1d.h"
+        int main(void){
+          printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(heat1d_opts), offsetof(heat1d_opts, stream),
+                 sizeof(heat1d_info_t), offsetof(heat1d_info_t, r), sizeof(heat1d_exchange_plan),
+                 offsetof(heat1d_opts, virtual_slabs));
+          return 0; }
+    """))
+    exe = tmp_path / "sz"
+    subprocess.check_call(["gcc", "-std=c99", "-I", os.path.dirname(HEADER), str(prog), "-o", str(exe)])
+    vals = list(map(int, subprocess.check_output([str(exe)], text=True).split()))
+    assert vals == [ctypes.sizeof(b.Opts), b.Opts.stream.offset, ctypes.sizeof(b.Info), b.Info.r.offset,
+                    ctypes.sizeof(b.ExchangePlan), b.Opts.virtual_slabs.offset]
+
+
+def test_defaults_and_strerror(lib):
+    import paper_2307_01117_b200 as h1
+    o = h1.default_opts()
+    assert o.size == ctypes.sizeof(o) and o.nranks == 1 and o.device == -1 and o.T == 0
+    assert o.virtual_slabs == 1 and o.blocking == 1
+    assert lib.heat1d_version() == 10000
+    assert h1.strerror(2).startswith("unstable")
+
+
+@pytest.mark.parametrize("args,status", [
+    ((0, 4, 10, 0.5, 1.0, 1.0), 1),            # nx < 1
+    ((10, 0, 10, 0.5, 1.0, 1.0), 1),           # np < 1
+    ((10, 4, -1, 0.5, 1.0, 1.0), 1),           # nt < 0
+    ((10, 4, 10, -0.1, 1.0, 1.0), 1),          # k < 0
+    ((10, 4, 10, 0.5, 0.0, 1.0), 1),           # dt <= 0
+    ((10, 4, 10, 0.5, 1.0, -1.0), 1),          # dx <= 0
+    ((10, 4, 10, float("nan"), 1.0, 1.0), 1),  # non-finite
+    ((10, 4, 10, 0.6, 1.0, 1.0), 2),           # r > 1/2
+    ((1 << 40, 1 << 30, 10, 0.5, 1.0, 1.0), 1),  # N > 2^62
+])
+def test_create_validation_without_gpu(lib, args, status):
+    import paper_2307_01117_b200 as h1
+    with pytest.raises(h1.Heat1DError) as ei:
+        h1.Heat1D(*args)
+    assert ei.value.status == status
+
+
+def test_bad_opts(lib):
+    import paper_2307_01117_b200 as h1
+    for kw, st in [(dict(T=33), 1), (dict(T=-1), 1), (dict(rank=2, nranks=2), 1), (dict(nranks=2), 1),
+                   (dict(virtual_slabs=0), 1), (dict(virtual_slabs=2, kernel="naive"), 7)]:
+        with pytest.raises(h1.Heat1DError) as ei:
+            h1.Heat1D(100, 4, 10, 0.25, 1.0, 1.0, **kw)
+        assert ei.value.status == st, kw
+
+
+def test_paper_2h_stability_uses_its_own_r(lib):
+    import paper_2307_01117_b200 as h1
+    # k=0.9: dx^2 mode r=0.9 unstable; paper 2h mode r=0.45 passes validation
+    # (and then fails only for lack of a GPU, with ECUDA -- not EUNSTABLE)
+    with pytest.raises(h1.Heat1DError) as ei:
+        h1.Heat1D(100, 4, 10, 0.9, 1.0, 1.0)
+    assert ei.value.status == 2
+    try:
+        h1.Heat1D(100, 4, 10, 0.9, 1.0, 1.0, denominator="paper_2dx")
+    except h1.Heat1DError as e:
+        assert e.status in (4, 5)
+
+
+@pytest.mark.parametrize("nx,np_,G", [(250, 4, 1), (250, 4, 2), (250, 4, 3), (10, 3, 4), (1 << 28, 8, 8),
+                                      (131072, 8, 4), (7, 1, 3), (5, 2, 4)])
+def test_partition_covers_ring(lib, nx, np_, G):
+    import paper_2307_01117_b200 as h1
+    N = nx * np_
+    slabs = [h1.partition(nx, np_, G, g) for g in range(G)]
+    pos = 0
+    for f, c in slabs:
+        assert f == pos and c >= 1
+        pos += c
+    assert pos == N
+    cs = [c for _, c in slabs]
+    if np_ >= G:
+        assert all(c % nx == 0 for c in cs)                  # whole partitions
+        assert max(cs) - min(cs) <= nx and cs == sorted(cs, reverse=True)  # front-loaded
+    else:
+        assert max(cs) - min(cs) <= 1
+
+
+def test_partition_spec_examples(lib):
+    import paper_2307_01117_b200 as h1
+    # SPEC.md:108-109 make_partition(10,3) -> [(0,4),(4,3),(7,3)], (9,3) -> even
+    assert [h1.partition(1, 10, 3, g) for g in range(3)] == [(0, 4), (4, 3), (7, 3)]
+    assert [h1.partition(1, 9, 3, g) for g in range(3)] == [(0, 3), (3, 3), (6, 3)]
+    with pytest.raises(h1.Heat1DError):          # SPEC.md:110 (5 cells, 8 slabs)
+        h1.partition(1, 5, 8, 0)
+
+
+def test_exchange_plan(lib):
+    import paper_2307_01117_b200 as h1
+    p = h1.plan_exchange(1 << 28, 8, 8, 0, 8)
+    assert (p.left, p.right) == (7, 1)
+    assert (p.send_right_off, p.send_left_off, p.recv_left_off, p.recv_right_off, p.cells) == \
+        ((1 << 28) - 8, 0, -8, 1 << 28, 8)
+    p = h1.plan_exchange(100, 2, 2, 1, 3)
+    assert (p.left, p.right) == (0, 0)
+    with pytest.raises(h1.Heat1DError):
+        h1.plan_exchange(4, 2, 2, 0, 5)              # halo deeper than a slab

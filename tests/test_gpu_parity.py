@@ -1,0 +1,296 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.  -m gpu.
+
+Matched mode must be BITWISE equal to the oracle (north_star: "bit-exact in
+matched-order mode"); fast mode within 1e-12*max|u0|*nt.  Inputs come from
+synth/ (seeded), expected values from oracle/ only.
+"""
+from __future__ import annotations
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth.configs import C1, C2, C3, C4, C5
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def h1():
+    import torch
+    from paper_2307_01117_b200 import _build
+    _build.build()
+    import paper_2307_01117_b200 as m
+    torch.cuda.set_device(0)
+    return m
+
+
+def gpu_run(h1, u0, nx, np_, nt, k, dt=1.0, dx=1.0, **kw):
+    with h1.Heat1D(nx, np_, nt, k, dt, dx, **kw) as h:
+        h.set_initial(u0)
+        h.run(nt)
+        return h.get()
+
+
+def assert_bitwise(got, want, what=""):
+    if not np.array_equal(got, want):
+        bad = np.flatnonzero(got != want)
+        raise AssertionError("%s: %d cells differ, first at %d: %r vs %r (max abs diff %g)" % (
+            what, bad.size, bad[0], got[bad[0]], want[bad[0]], np.max(np.abs(got - want))))
+
+
+# ------------------------------------------------------------------ C1
+@pytest.mark.parametrize("T", [0, 1, 2, 3, 4, 5, 8, 12, 16, 31, 32])
+def test_c1_bitwise_all_T(h1, T):
+    r = oracle.r_of(C1.k, C1.dt, C1.dx)
+    want = oracle.run(C1.u0(), r, C1.nt)
+    got = gpu_run(h1, C1.u0(), C1.nx, C1.np, C1.nt, C1.k, T=T)
+    assert_bitwise(got, want, "C1 T=%d" % T)
+
+
+def test_c1_naive_kernel(h1):
+    want = oracle.run(C1.u0(), 0.5, C1.nt)
+    assert_bitwise(gpu_run(h1, C1.u0(), C1.nx, C1.np, C1.nt, C1.k, kernel="naive"), want, "C1 naive")
+
+
+# ------------------------------------------------------------------ degenerate rings
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 6, 7, 8, 13, 31, 33])
+@pytest.mark.parametrize("k", [0.25, 0.5, 0.4])
+@pytest.mark.parametrize("T", [1, 2, 8])
+def test_tiny_rings(h1, N, k, T):
+    u0 = synth.uniform(N, 0, N, -1.0, 1.0)
+    nt = 17
+    want = oracle.run(u0, k, nt)
+    assert_bitwise(gpu_run(h1, u0, N, 1, nt, k, T=T), want, "N=%d" % N)
+
+
+def test_zero_diffusivity_identity(h1):
+    u0 = synth.uniform(3, 0, 5000)
+    assert_bitwise(gpu_run(h1, u0, 5000, 1, 10, 0.0, T=4), u0, "k=0")
+
+
+# ------------------------------------------------------------------ ragged, several tiles
+@pytest.mark.parametrize("N", [4097, 100_003, (1 << 20) + 7])
+@pytest.mark.parametrize("T", [1, 3, 8, 12])
+@pytest.mark.parametrize("k", [0.4, 0.5])
+def test_ragged_multi_tile(h1, N, T, k):
+    nt = 2 * T + 3           # full passes + a tail pass
+    u0 = synth.uniform(N + T, 0, N, -1.0, 1.0)
+    want = oracle.run(u0, k, nt)
+    assert_bitwise(gpu_run(h1, u0, N, 1, nt, k, T=T), want, "N=%d T=%d" % (N, T))
+
+
+@pytest.mark.parametrize("geom", ["9,4,3,4", "9,8,4,2", "17,4,4,2", "17,8,2,1", "17,8,3,2", "17,8,4,1",
+                                  "25,4,3,2", "25,8,3,1", "33,4,3,2", "33,8,3,1"])
+def test_all_pass_geometries(h1, geom, monkeypatch):
+    monkeypatch.setenv("HEAT1D_GEOM", geom)
+    N, nt = 300_001, 29
+    u0 = synth.uniform(77, 0, N, -1.0, 1.0)
+    for k, T in [(0.4, 7), (0.5, 12)]:
+        want = oracle.run(u0, k, nt)
+        assert_bitwise(gpu_run(h1, u0, N, 1, nt, k, T=T), want, "geom %s T=%d" % (geom, T))
+
+
+# ------------------------------------------------------------------ C2 (paper's workload size)
+def test_c2_bitwise_and_conservation(h1):
+    r = oracle.r_of(C2.k, C2.dt, C2.dx)
+    u0 = C2.u0()
+    want = oracle.run(u0, r, C2.nt)
+    got = gpu_run(h1, u0, C2.nx, C2.np, C2.nt, C2.k)
+    assert_bitwise(got, want, "C2")
+    assert abs(math.fsum(got) - math.fsum(u0)) <= 1e-9 * math.fsum(np.abs(u0))
+
+
+def test_c2_nx_np_invariance(h1):
+    """(nx, np) only changes the partitioning: identical bits for every split
+    (single slab, and as virtual slabs = partitions grouped per 'GPU')."""
+    u0 = C2.u0()
+    ref = gpu_run(h1, u0, C2.nx, C2.np, C2.nt, C2.k)
+    for nx, np_, vs in [(1_000_000, 1, 1), (1000, 1000, 1), (250, 4000, 1), (10_000, 100, 4), (1000, 1000, 8),
+                        (250, 4000, 3)]:
+        assert_bitwise(gpu_run(h1, u0, nx, np_, C2.nt, C2.k, virtual_slabs=vs), ref, "nx=%d np=%d vs=%d" % (nx, np_, vs))
+
+
+# ------------------------------------------------------------------ invariances of the GPU path
+def test_cross_T_bitwise(h1):
+    N, nt = 1 << 20, 96
+    u0 = synth.uniform(5, 0, N, -1.0, 1.0)
+    ref = gpu_run(h1, u0, N, 1, nt, 0.4, kernel="naive")
+    for T in [1, 2, 3, 4, 6, 8, 11, 12, 16, 24, 32]:
+        assert_bitwise(gpu_run(h1, u0, N, 1, nt, 0.4, T=T), ref, "T=%d" % T)
+
+
+def test_split_run_invariance(h1):
+    N = 200_000
+    u0 = synth.uniform(9, 0, N, -1.0, 1.0)
+    with h1.Heat1D(N, 1, 0, 0.4, 1.0, 1.0, T=8) as h:
+        h.set_initial(u0)
+        h.run(13)
+        h.run(0)
+        h.run(29)
+        assert h.steps_done == 42
+        got = h.get()
+    assert_bitwise(got, oracle.run(u0, 0.4, 42), "split")
+
+
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
+@pytest.mark.parametrize("T", [1, 4, 8, 12])
+def test_virtual_slabs_multi_gpu_schedule(h1, G, T):
+    """The multi-GPU schedule (exchange || interior, then edges) with the
+    transport replaced by device copies between G slabs on one GPU."""
+    nx, np_ = 12_289, 8
+    nt = 3 * T + 1
+    u0 = synth.uniform(G * 100 + T, 0, nx * np_, -1.0, 1.0)
+    want = oracle.run(u0, 0.4, nt)
+    assert_bitwise(gpu_run(h1, u0, nx, np_, nt, 0.4, T=T, virtual_slabs=G), want, "G=%d T=%d" % (G, T))
+
+
+def test_virtual_slabs_small_slabs(h1):
+    # slabs of 5 cells with T clamped to the slab size
+    u0 = synth.uniform(1, 0, 20)
+    want = oracle.run(u0, 0.5, 40)
+    assert_bitwise(gpu_run(h1, u0, 5, 4, 40, 0.5, T=8, virtual_slabs=4), want, "tiny slabs")
+
+
+# ------------------------------------------------------------------ fast mode bound
+def test_fast_mode_within_bound(h1):
+    N, nt = 1_000_000, 1000
+    u0 = synth.uniform(42, 0, N, -1.0, 1.0)
+    want = oracle.run(u0, 0.4, nt)
+    got = gpu_run(h1, u0, N, 1, nt, 0.4, mode="fast")
+    err = np.max(np.abs(got - want))
+    assert err <= 1e-12 * np.max(np.abs(u0)) * nt, err
+
+
+def test_paper_2h_denominator(h1):
+    # literal Eq. 2: r = k*dt/(2 dx); k=0.8, dx=1 -> r = 0.4
+    u0 = synth.uniform(2, 0, 5000)
+    want = oracle.run(u0, oracle.r_of(0.8, 1.0, 1.0, paper_2h=True), 50)
+    assert_bitwise(gpu_run(h1, u0, 5000, 1, 50, 0.8, denominator="paper_2dx"), want, "2h")
+
+
+# ------------------------------------------------------------------ boundary semantics
+def test_init_uniform_matches_synth(h1):
+    N = 1_000_003
+    with h1.Heat1D(N, 1, 0, 0.5, 1.0, 1.0) as h:
+        h.init_uniform(1234, -1.0, 1.0)
+        got = h.get()
+    assert_bitwise(got, synth.uniform(1234, 0, N, -1.0, 1.0), "K0")
+    with h1.Heat1D(1000, 8, 0, 0.5, 1.0, 1.0, virtual_slabs=8) as h:
+        h.init_uniform(42)
+        assert_bitwise(h.get(), synth.uniform(42, 0, 8000), "K0 slabs")
+
+
+def test_state_errors_and_ownership(h1):
+    import torch
+    with h1.Heat1D(1000, 1, 5, 0.5, 1.0, 1.0) as h:
+        with pytest.raises(h1.Heat1DError) as ei:
+            h.run()
+        assert ei.value.status == 3                       # ESTATE
+        with pytest.raises(h1.Heat1DError):
+            h.get()
+        u0 = synth.uniform(4, 0, 1000)
+        buf = u0.copy()
+        h.set_initial(buf)
+        buf[:] = np.nan                                   # copy made: caller may reuse
+        assert_bitwise(h.get(), u0, "get before run")
+        h.run(0)
+        assert h.steps_done == 0
+        with pytest.raises(h1.Heat1DError) as ei:
+            h.set_initial(u0[:10])
+        assert ei.value.status == 1
+        # device pointers in and out
+        d = torch.from_numpy(u0).cuda()
+        h.set_initial(d)
+        h.run()
+        out = torch.empty(1000, dtype=torch.float64, device="cuda")
+        h.get(out)
+        assert_bitwise(out.cpu().numpy(), oracle.run(u0, 0.5, 5), "device ptrs")
+        info = h.info()
+        assert info["steps_done"] == 5 and info["N"] == 1000 and info["dp_ops"] == 3
+
+
+def test_unstable_allowed(h1):
+    u0 = synth.uniform(8, 0, 256)
+    want = oracle.run(u0, 0.6, 5)
+    assert_bitwise(gpu_run(h1, u0, 256, 1, 5, 0.6, allow_unstable=True, T=2), want, "r=0.6")
+
+
+# ------------------------------------------------------------------ full-size configs
+def test_c5_full_bitwise_and_closed_form(h1):
+    """C5 in full (2^20 cells, 20000 steps, r=1/4) vs O1 bitwise, plus the
+    closed-form decay of the single mode m=5 (BASELINE.json configs[4])."""
+    u0 = C5.u0()
+    r = oracle.r_of(C5.k, C5.dt, C5.dx)
+    got = gpu_run(h1, u0, C5.nx, C5.np, C5.nt, C5.k)
+    s = math.sin(math.pi * 5 / C5.N)
+    g_t = math.exp(C5.nt * math.log1p(-4.0 * r * s * s))
+    assert np.max(np.abs(got - g_t * u0)) <= 1e-12
+    assert_bitwise(got, oracle.run(u0, r, C5.nt), "C5")
+    got8 = gpu_run(h1, u0, C5.nx, C5.np, C5.nt, C5.k, virtual_slabs=8)
+    assert_bitwise(got8, got, "C5 8 virtual slabs")
+
+
+def test_c3_full_windows_and_closed_form(h1):
+    """C3 at full size (2^28 cells, nt=1000, r=0.4): O3 windows bitwise at
+    tile/partition edges and the wrap, and the 8-mode closed form on a
+    strided sample of every cell class (BASELINE.json configs[2])."""
+    import torch
+    N, nt = C3.N, C3.nt
+    r = oracle.r_of(C3.k, C3.dt, C3.dx)
+    u0 = C3.u0()
+    out = torch.empty(N, dtype=torch.float64, device="cuda")
+    with h1.Heat1D(C3.nx, C3.np, nt, C3.k, C3.dt, C3.dx) as h:
+        h.set_initial(u0)
+        tile = h.info()["tile_cells"]
+        h.run()
+        h.get(out)
+    got = out.cpu().numpy()
+    rng = np.random.default_rng(0)
+    starts = [0, N - 64, C3.nx - 100, 5 * C3.nx - 3, tile - 50, 7 * tile - 1] + list(rng.integers(0, N - 600, 10))
+    for a in starts:
+        b = a + 512
+        w = oracle.window(C3.u0(a - nt, b - a + 2 * nt), nt, r)
+        idx = np.arange(a, b) % N
+        assert_bitwise(got[idx], w, "C3 window %d" % a)
+    # closed form on every 97th cell
+    sel = np.arange(0, N, 97, dtype=np.int64)
+    want = np.zeros(sel.size)
+    for m, a in zip(C3.modes, C3.amps()):
+        s = math.sin(math.pi * m / N)
+        gt = math.exp(nt * math.log1p(-4.0 * r * s * s))
+        want += a * gt * np.sin(2.0 * np.pi * ((m * sel) % N) / N)
+    assert np.max(np.abs(got[sel] - want)) <= 1e-12
+
+
+def test_c4_first_100_steps_windows(h1):
+    """C4 (2^31 cells, 16 GiB) on one GPU: the first 100 steps checked with O3
+    windows at all 8 slab boundaries, the wrap and random cells, both as one
+    slab and as 8 virtual slabs (the 8-GPU decomposition); the two agree
+    bitwise everywhere (BASELINE.json configs[3])."""
+    import torch
+    N, nt = C4.N, 100
+    r = oracle.r_of(C4.k, C4.dt, C4.dx)
+    out = torch.empty(N, dtype=torch.float64, device="cuda")
+    with h1.Heat1D(C4.nx, C4.np, nt, C4.k, C4.dt, C4.dx) as h:
+        h.init_uniform(C4.seed, C4.lo, C4.hi)
+        h.run()
+        h.get(out)
+    rng = np.random.default_rng(1)
+    starts = [g * C4.nx - 256 for g in range(8)] + list(rng.integers(0, N - 600, 8))
+    got = {}
+    for a in starts:
+        idx = (np.arange(a, a + 512) % N).astype(np.int64)
+        got[a] = out[torch.from_numpy(idx).cuda()].cpu().numpy()
+        w = oracle.window(C4.u0(a - nt, 512 + 2 * nt), nt, r)
+        assert_bitwise(got[a], w, "C4 window %d" % a)
+    with h1.Heat1D(C4.nx, C4.np, nt, C4.k, C4.dt, C4.dx, virtual_slabs=8) as h:
+        h.init_uniform(C4.seed, C4.lo, C4.hi)
+        h.run()
+        out2 = torch.empty(N, dtype=torch.float64, device="cuda")
+        h.get(out2)
+    assert torch.equal(out, out2)
