@@ -56,7 +56,7 @@ struct heat1d_s {
     int64_t steps_done = 0;
     int64_t launches = 0;
     int num_sms = 148;
-    PassGeom geom{17, 8, 3, 2};
+    PassGeom geom{17, 8, 3, 2, 2};
     int last_grid = 0;
 
     cudaStream_t stream = nullptr, comm = nullptr;
@@ -154,17 +154,19 @@ int64_t min_slab(int64_t nx, int64_t np, int32_t G) {
 }
 
 int auto_T(int ops) {
-    // 4-op (matched, general r) is HBM-bound up to T~11 on B200;
-    // 3-op reaches the fp64 issue limit later.  Overridable via opts.T.
-    return ops == 4 ? 8 : 12;
+    // the largest T whose sustained (power-capped) throughput stays
+    // >= 70% of the HBM roofline 409*T GLUPS: 10 for the 4-op arithmetic
+    // (general r), 12 for the 3-op one (r a power of two, or fast mode).
+    return ops == 4 ? 10 : 12;
 }
 
 bool parse_geom_env(PassGeom *g) {
-    const char *s = getenv("HEAT1D_GEOM");  // "V,NW,S,ctas_per_sm" (tuning knob)
+    const char *s = getenv("HEAT1D_GEOM");  // "V,NW,S,ctas_per_sm[,kind]" (tuning knob)
     if (!s || !*s) return false;
-    int v, nw, st, c;
-    if (sscanf(s, "%d,%d,%d,%d", &v, &nw, &st, &c) != 4) return false;
-    *g = PassGeom{v, nw, st, c};
+    int v, nw, st, c, kind = 1;
+    const int got = sscanf(s, "%d,%d,%d,%d,%d", &v, &nw, &st, &c, &kind);
+    if (got < 4) return false;
+    *g = PassGeom{v, nw, st, c, kind};
     return true;
 }
 

@@ -38,6 +38,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
                  : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
@@ -97,6 +101,36 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 constexpr unsigned FULL = 0xffffffffu;
 
 }  // namespace
+
+// One Jacobi step of a warp-row of 32*V cells held V per lane: u -> v.
+// The two inter-lane neighbours come by shuffle (issued first, consumed last);
+// the cells of the warp's two outermost lanes go stale by one cell per step.
+template <int V, int OPS>
+__device__ __forceinline__ void warp_step(const double (&u)[V], double (&v)[V], double r) {
+    const double L = __shfl_up_sync(0xffffffffu, u[V - 1], 1);
+    const double R = __shfl_down_sync(0xffffffffu, u[0], 1);
+#pragma unroll
+    for (int j = 1; j < V - 1; ++j) v[j] = eq2<OPS>(u[j - 1], u[j], u[j + 1], r);
+    v[0] = eq2<OPS>(L, u[0], u[1], r);
+    v[V - 1] = eq2<OPS>(u[V - 2], u[V - 1], R, r);
+}
+
+// T steps in registers, ping-pong between u and a scratch array (no moves
+// inside the loop); the result is left in u.
+template <int V, int OPS>
+__device__ __forceinline__ void warp_steps(double (&u)[V], int T, double r) {
+    double v[V];
+    int s = 0;
+    for (; s + 2 <= T; s += 2) {
+        warp_step<V, OPS>(u, v, r);
+        warp_step<V, OPS>(v, u, r);
+    }
+    if (s < T) {
+        warp_step<V, OPS>(u, v, r);
+#pragma unroll
+        for (int j = 0; j < V; ++j) u[j] = v[j];
+    }
+}
 
 // ------------------------------------------------------------------ K2
 //
@@ -175,18 +209,7 @@ k2_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, 
 
         __syncthreads();  // B1: every warp has its span in registers -> in-place writes are safe
 
-        for (int step = 0; step < T; ++step) {
-            const double L = __shfl_up_sync(FULL, u[V - 1], 1);
-            const double R = __shfl_down_sync(FULL, u[0], 1);
-            double prev = L;
-#pragma unroll
-            for (int j = 0; j < V; ++j) {
-                const double b = u[j];
-                const double c = (j + 1 < V) ? u[j + 1] : R;
-                u[j] = eq2<OPS>(prev, b, c, r);
-                prev = b;
-            }
-        }
+        warp_steps<V, OPS>(u, T, r);
 
 #pragma unroll
         for (int j = 0; j < V; ++j) {
@@ -219,10 +242,231 @@ k2_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, 
     if (tid == 0) bulk_wait<0>();
 }
 
+// ------------------------------------------------------------------ K2 (warp-autonomous)
+//
+// Same arithmetic and the same per-warp trapezoid as k2_pass, but every warp
+// owns an S-slot TMA ring of 32V-cell spans and its own mbarriers: lane 0
+// issues the bulk load of the span [x0-T, x0+OW+T) and, after the warp has
+// written its OW = 32V-2T exact outputs back into the slot, the bulk store.
+// No CTA-wide barrier exists, so warps never wait for each other.  Adjacent
+// global warps take adjacent spans, so the 2T-cell overlaps hit in L2.
+template <int V, int NW, int S, int OPS>
+__global__ void __launch_bounds__(NW * 32)
+k2w_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t out_lo,
+         int64_t out_hi, int wrapT, double r, int64_t nspans, uint32_t slot_doubles) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int BAR_BYTES = ((NW * S * 8 + 127) / 128) * 128;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw) + warp * S;
+    double *slots = reinterpret_cast<double *>(smem_raw + BAR_BYTES) + (size_t)warp * S * slot_doubles;
+
+    const int OW = 32 * V - 2 * T;
+    const int64_t stride = (int64_t)gridDim.x * NW;
+    const int64_t first = (int64_t)blockIdx.x * NW + warp;
+    const uint64_t pol_in = policy_evict_first();
+
+    if (lane == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+
+    auto issue_load = [&](int64_t sp, int s) {
+        const int64_t x0 = out_lo + sp * OW;
+        const int64_t x1 = min(x0 + OW, out_hi);
+        const int64_t lo = x0 - T;
+        const int64_t ld_lo = lo - (lo & 1);
+        int64_t ld_hi = x1 + T;
+        ld_hi += (ld_hi & 1);
+        const uint32_t bytes = (uint32_t)((ld_hi - ld_lo) * 8);
+        mbar_arrive_expect_tx(&bars[s], bytes);
+        bulk_g2s(slots + (size_t)s * slot_doubles, A + ld_lo, bytes, &bars[s], pol_in);
+    };
+
+    if (lane == 0) {
+        for (int i = 0; i < S - 1; ++i) {
+            const int64_t sp = first + i * stride;
+            if (sp >= nspans) break;
+            issue_load(sp, i);
+        }
+    }
+
+    int k = 0;
+    for (int64_t sp = first; sp < nspans; sp += stride, ++k) {
+        const int s = k % S;
+        const uint32_t parity = (uint32_t)((k / S) & 1);
+        double *st = slots + (size_t)s * slot_doubles;
+        const int64_t x0 = out_lo + sp * OW;
+        const int64_t x1 = min(x0 + OW, out_hi);
+        const int64_t lo = x0 - T;
+        const int sh = (int)(lo & 1);
+        const int64_t ld_lo = lo - sh;
+
+        mbar_wait(&bars[s], parity);
+        const int base = sh + lane * V;
+        double u[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) u[j] = st[base + j];
+
+        warp_steps<V, OPS>(u, T, r);
+
+        // each lane rewrites only its own cells: no intra-warp WAR hazard
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const int p = lane * V + j;
+            if (p >= T && p < 32 * V - T) st[base + j] = u[j];
+        }
+        fence_proxy_async();
+        __syncwarp();
+
+        if (lane == 0) {
+            const int64_t a = x0 + (x0 & 1);
+            const int64_t b = x1 - (x1 & 1);
+            if (b > a) bulk_s2g(B + a, st + (a - ld_lo), (uint32_t)((b - a) * 8));
+            bulk_commit();
+            const int64_t nxt = sp + (int64_t)(S - 1) * stride;
+            if (nxt < nspans) {
+                bulk_wait_read<1>();
+                fence_proxy_async();
+                issue_load(nxt, (k + S - 1) % S);
+            }
+            if (x0 & 1) B[x0] = st[x0 - ld_lo];
+        }
+        if (lane == 1 && (x1 & 1) && x1 - 1 >= x0) B[x1 - 1] = st[x1 - 1 - ld_lo];
+        for (int j = lane; j < wrapT; j += 32) {
+            if (j >= x0 && j < x1) B[n + j] = st[j - ld_lo];
+            const int64_t c = n - wrapT + j;
+            if (c >= x0 && c < x1) B[j - wrapT] = st[c - ld_lo];
+        }
+    }
+    if (lane == 0) bulk_wait<0>();
+}
+
+// ------------------------------------------------------------------ K2 (warp-specialised)
+//
+// k2_pass with a dedicated producer warp: warps 0..NW-1 compute, warp NW owns
+// all TMA traffic.  The producer refills a stage as soon as the bulk store of
+// its previous tile has read it out, so S-1 loads are in flight while the
+// compute warps work; compute warps never wait for stores, and their only
+// CTA-level sync is a named barrier (B1) among themselves before the in-place
+// write-back.  Per stage: full[s] (TMA complete_tx) and done[s] (NW arrivals).
+template <int V, int NW, int S, int OPS>
+__global__ void __launch_bounds__((NW + 1) * 32)
+k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t out_lo,
+         int64_t out_hi, int wrapT, double r, int64_t ntiles, uint32_t stage_doubles) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);
+    uint64_t *done = full + S;
+    double *stages = reinterpret_cast<double *>(smem_raw + 128);
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int OW = 32 * V - 2 * T;
+    const int64_t W = (int64_t)NW * OW;
+    const int64_t stride = gridDim.x;
+
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&done[s], NW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == NW) {
+        // ---------------- producer warp
+        const uint64_t pol_in = policy_evict_first();
+        auto issue_load = [&](int64_t tile, int s) {
+            const int64_t x0 = out_lo + tile * W;
+            const int64_t x1 = min(x0 + W, out_hi);
+            const int64_t lo = x0 - T;
+            const int64_t ld_lo = lo - (lo & 1);
+            int64_t ld_hi = x1 + T;
+            ld_hi += (ld_hi & 1);
+            const uint32_t bytes = (uint32_t)((ld_hi - ld_lo) * 8);
+            mbar_arrive_expect_tx(&full[s], bytes);
+            bulk_g2s(stages + (size_t)s * stage_doubles, A + ld_lo, bytes, &full[s], pol_in);
+        };
+        if (lane == 0) {
+            for (int i = 0; i < S; ++i) {
+                const int64_t tile = blockIdx.x + i * stride;
+                if (tile >= ntiles) break;
+                issue_load(tile, i);
+            }
+        }
+        int k = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += stride, ++k) {
+            const int s = k % S;
+            double *st = stages + (size_t)s * stage_doubles;
+            const int64_t x0 = out_lo + tile * W;
+            const int64_t x1 = min(x0 + W, out_hi);
+            const int64_t lo = x0 - T;
+            const int64_t ld_lo = lo - (lo & 1);
+            mbar_wait(&done[s], (uint32_t)((k / S) & 1));
+            // scalar leftovers: an odd first/last cell and the periodic self-halo
+            if (lane == 0 && (x0 & 1)) B[x0] = st[x0 - ld_lo];
+            if (lane == 1 && (x1 & 1) && x1 - 1 >= x0) B[x1 - 1] = st[x1 - 1 - ld_lo];
+            for (int j = lane; j < wrapT; j += 32) {
+                if (j >= x0 && j < x1) B[n + j] = st[j - ld_lo];
+                const int64_t c = n - wrapT + j;
+                if (c >= x0 && c < x1) B[j - wrapT] = st[c - ld_lo];
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const int64_t a = x0 + (x0 & 1);
+                const int64_t b = x1 - (x1 & 1);
+                if (b > a) bulk_s2g(B + a, st + (a - ld_lo), (uint32_t)((b - a) * 8));
+                bulk_commit();
+                const int64_t nxt = tile + (int64_t)S * stride;
+                if (nxt < ntiles) {
+                    bulk_wait_read<0>();  // tile's bytes have left the stage
+                    fence_proxy_async();
+                    issue_load(nxt, s);
+                }
+            }
+            __syncwarp();
+        }
+        if (lane == 0) bulk_wait<0>();
+        return;
+    }
+
+    // ---------------- compute warps
+    int k = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += stride, ++k) {
+        const int s = k % S;
+        double *st = stages + (size_t)s * stage_doubles;
+        const int64_t x0 = out_lo + tile * W;
+        const int sh = (int)((x0 - T) & 1);
+        mbar_wait(&full[s], (uint32_t)((k / S) & 1));
+        const int base = sh + warp * OW + lane * V;
+        double u[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) u[j] = st[base + j];
+        asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");  // B1 among compute warps
+        warp_steps<V, OPS>(u, T, r);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const int p = lane * V + j;
+            if (p >= T && p < 32 * V - T) st[base + j] = u[j];
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&done[s]);
+    }
+}
+
 size_t PassGeom::smem_bytes(int T) const {
-    const int64_t in_cells = tile_out(T) + 2 * T + 2;
-    const int64_t stage = (in_cells + 15) / 16 * 16;
-    return 128 + (size_t)S * (size_t)stage * sizeof(double);
+    if (kind == 0 || kind == 2) {
+        const int64_t in_cells = tile_out(T) + 2 * T + 2;
+        const int64_t stage = (in_cells + 15) / 16 * 16;
+        return 128 + (size_t)S * (size_t)stage * sizeof(double);
+    }
+    const int64_t slot = (32 * (int64_t)V + 2 + 15) / 16 * 16;
+    const size_t bar = (size_t)((NW * S * 8 + 127) / 128) * 128;
+    return bar + (size_t)NW * S * (size_t)slot * sizeof(double);
 }
 
 namespace {
@@ -231,17 +475,21 @@ using PassFn = void (*)(const double *, double *, int64_t, int, int64_t, int64_t
                         uint32_t);
 
 template <int V, int NW, int S, int OPS>
-PassFn pass_fn() {
-    return &k2_pass<V, NW, S, OPS>;
+PassFn pass_fn(int kind) {
+    return kind == 0 ? &k2_pass<V, NW, S, OPS> : kind == 1 ? &k2w_pass<V, NW, S, OPS> : &k2p_pass<V, NW, S, OPS>;
 }
 
+// (V, NW, S) instantiated for both kernel kinds and both arithmetic variants.
 #define HEAT1D_GEOMS(X)                                                                            \
-    X(9, 4, 3) X(9, 4, 4) X(9, 8, 3) X(9, 8, 4) X(17, 4, 3) X(17, 4, 4) X(17, 8, 2) X(17, 8, 3)  \
-    X(17, 8, 4) X(25, 4, 3) X(25, 4, 4) X(25, 8, 3) X(25, 8, 4) X(33, 4, 3) X(33, 8, 3)
+    X(9, 4, 3) X(9, 4, 4) X(9, 8, 3) X(9, 8, 4) X(17, 4, 2) X(17, 4, 3) X(17, 4, 4) X(17, 8, 2)  \
+    X(17, 8, 3) X(17, 8, 4) X(21, 4, 3) X(21, 8, 3) X(25, 4, 2) X(25, 4, 3) X(25, 4, 4) X(25, 8, 2) \
+    X(25, 8, 3) X(25, 8, 4) X(33, 4, 2) X(33, 4, 3) X(33, 8, 2) X(33, 8, 3) X(15, 8, 2) X(15, 8, 3)   \
+    X(17, 6, 2) X(17, 6, 3) X(17, 12, 2) X(17, 16, 2)
 
-PassFn lookup_pass(int V, int NW, int S, int ops) {
+PassFn lookup_pass(int V, int NW, int S, int ops, int kind) {
 #define X(v, nw, s)                                                                                \
-    if (V == v && NW == nw && S == s) return ops == 4 ? pass_fn<v, nw, s, 4>() : pass_fn<v, nw, s, 3>();
+    if (V == v && NW == nw && S == s)                                                              \
+        return ops == 4 ? pass_fn<v, nw, s, 4>(kind) : pass_fn<v, nw, s, 3>(kind);
     HEAT1D_GEOMS(X)
 #undef X
     return nullptr;
@@ -250,54 +498,61 @@ PassFn lookup_pass(int V, int NW, int S, int ops) {
 }  // namespace
 
 PassGeom choose_geom(int64_t n_out, int T, int num_sms) {
-    // Default: V=17 (odd), 8 compute warps, 3 stages, 2 CTAs per SM (16 warps/SM,
-    // ~2 x 104 KB of the 228 KB shared memory).  Small rings get smaller tiles so
-    // that every SM has work.
-    PassGeom g{17, 8, 3, 2};
-    const int64_t want_tiles = (int64_t)num_sms * g.ctas_per_sm;
-    if (n_out < want_tiles * g.tile_out(T)) g = PassGeom{9, 4, 4, 4};
+    // Default: CTA tiles of 8 compute warps x V=17 cells/lane plus
+    // a TMA producer warp, 3 stages (~100 KB), 2 CTAs per SM.  Rings too small
+    // to give every CTA a tile use 4-warp tiles of V=9.
+    PassGeom g{17, 8, 3, 2, 2};
+    if (n_out < (int64_t)num_sms * g.ctas_per_sm * g.tile_out(T)) g = PassGeom{9, 4, 3, 4, 2};
     return g;
 }
 
 cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, int64_t n, int T,
                         int64_t out_lo, int64_t out_hi, int wrapT, double r, int num_sms,
                         cudaStream_t st, int *grid_out) {
-    PassFn fn = lookup_pass(g.V, g.NW, g.S, ops);
+    PassFn fn = lookup_pass(g.V, g.NW, g.S, ops, g.kind);
     if (!fn) return cudaErrorInvalidConfiguration;
     if (out_hi <= out_lo) {
         if (grid_out) *grid_out = 0;
         return cudaSuccess;
     }
     const int64_t W = g.tile_out(T);
-    if (W <= 0) return cudaErrorInvalidValue;
-    const int64_t ntiles = (out_hi - out_lo + W - 1) / W;
+    if (W <= 0 || 32 * g.V - 2 * T <= 0) return cudaErrorInvalidValue;
+    const int64_t units = (out_hi - out_lo + W - 1) / W;
     const size_t smem = g.smem_bytes(T);
-    const int64_t in_cells = W + 2 * T + 2;
+    const int64_t in_cells = (g.kind != 1 ? W : 32 * (int64_t)g.V - 2 * T) + 2 * T + 2;
     const uint32_t stage_doubles = (uint32_t)((in_cells + 15) / 16 * 16);
     // Raise the dynamic shared-memory limit once per instantiation (max over T).
     {
         static std::mutex mu;
-        static size_t done_bytes[64] = {0};
-        static PassFn done_fn[64] = {nullptr};
+        static PassFn done_fn[256] = {nullptr};
         std::lock_guard<std::mutex> lk(mu);
+        bool done = false;
         int slot = -1;
-        for (int i = 0; i < 64; ++i) {
-            if (done_fn[i] == fn) { slot = i; break; }
+        for (int i = 0; i < 256; ++i) {
+            if (done_fn[i] == fn) { done = true; break; }
             if (done_fn[i] == nullptr) { slot = i; break; }
         }
-        if (slot >= 0 && (done_fn[slot] != fn || done_bytes[slot] < smem)) {
+        if (!done) {
             const size_t want = g.smem_bytes(1);  // the largest tile (T=1)
             cudaError_t e = cudaFuncSetAttribute((const void *)fn,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
             if (e != cudaSuccess) return e;
-            done_fn[slot] = fn;
-            done_bytes[slot] = want;
+            if (slot >= 0) done_fn[slot] = fn;
         }
     }
-    int64_t grid = (int64_t)num_sms * g.ctas_per_sm;
-    if (grid > ntiles) grid = ntiles;
+    // Persistent grid: never more CTAs than can be co-resident (static round-robin
+    // assignment assumes a single wave).
+    int occ = 0;
+    const int threads = (g.NW + (g.kind == 2 ? 1 : 0)) * 32;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)fn, threads, smem) != cudaSuccess ||
+        occ < 1)
+        occ = 1;
+    const int per_sm = g.ctas_per_sm < occ ? g.ctas_per_sm : occ;
+    int64_t grid = (int64_t)num_sms * per_sm;
+    const int64_t need = g.kind != 1 ? units : (units + g.NW - 1) / g.NW;
+    if (grid > need) grid = need;
     if (grid_out) *grid_out = (int)grid;
-    fn<<<(unsigned)grid, g.NW * 32, smem, st>>>(A, B, n, T, out_lo, out_hi, wrapT, r, ntiles, stage_doubles);
+    fn<<<(unsigned)grid, threads, smem, st>>>(A, B, n, T, out_lo, out_hi, wrapT, r, units, stage_doubles);
     return cudaGetLastError();
 }
 

@@ -13,10 +13,14 @@ enum Ops { OPS_MATCHED4 = 4, OPS_FMA3 = 3 };
 struct PassGeom {
     int V;            // cells per thread (odd: conflict-free 64-bit LDS/STS)
     int NW;           // compute warps per CTA
-    int S;            // TMA pipeline stages
-    int ctas_per_sm;  // resident CTAs per SM the config is sized for
+    int S;            // TMA pipeline stages (per CTA for kind 0, per warp for kind 1)
+    int ctas_per_sm;  // resident CTAs per SM the config is sized for (capped by occupancy)
+    int kind = 1;     // 0: CTA tiles (one TMA copy per CTA tile, 2 CTA barriers per tile)
+                      // 1: warp-autonomous spans (each warp its own TMA ring; no CTA barriers)
+                      // 2: CTA tiles + a dedicated TMA producer warp (NW+1 warps per CTA)
     size_t smem_bytes(int T) const;
-    int64_t tile_out(int T) const { return (int64_t)NW * (32 * V - 2 * T); }
+    // output cells per scheduling unit (a CTA tile for kind 0, a warp span for kind 1)
+    int64_t tile_out(int T) const { return (kind != 1 ? (int64_t)NW : 1) * (32 * V - 2 * T); }
 };
 
 // Pick the pass-kernel configuration for (n, T).

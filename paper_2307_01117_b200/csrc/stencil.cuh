@@ -30,4 +30,18 @@ __device__ __forceinline__ double eq2(double a, double b, double c, double r) {
     }
 }
 
+// The same three (or four) operations split into phases so that a thread can
+// issue one phase for all of its V cells before the next: consecutive
+// dependent operations are then V instructions apart, which hides the fp64
+// pipe latency without relying on other warps.  eq2 == p3(p2(p1(a,b),c),b,r).
+__device__ __forceinline__ double eq2_p1(double a, double b) { return __fma_rn(-2.0, b, a); }
+__device__ __forceinline__ double eq2_p2(double t, double c) { return __dadd_rn(t, c); }
+template <int OPS>
+__device__ __forceinline__ double eq2_p3(double t, double b, double r) {
+    if constexpr (OPS == 4)
+        return __dadd_rn(b, __dmul_rn(r, t));
+    else
+        return __fma_rn(r, t, b);
+}
+
 }  // namespace heat1d

@@ -84,8 +84,12 @@ def test_ragged_multi_tile(h1, N, T, k):
     assert_bitwise(gpu_run(h1, u0, N, 1, nt, k, T=T), want, "N=%d T=%d" % (N, T))
 
 
-@pytest.mark.parametrize("geom", ["9,4,3,4", "9,8,4,2", "17,4,4,2", "17,8,2,1", "17,8,3,2", "17,8,4,1",
-                                  "25,4,3,2", "25,8,3,1", "33,4,3,2", "33,8,3,1"])
+@pytest.mark.parametrize("geom", ["9,4,3,4,0", "9,8,4,2,0", "17,4,4,2,0", "17,8,2,1,0", "17,8,3,2,0",
+                                  "25,4,3,2,0", "33,8,3,1,0",
+                                  "9,4,3,4,1", "9,8,4,2,1", "17,4,2,4,1", "17,8,3,2,1", "17,8,2,2,1",
+                                  "21,8,3,1,1", "25,4,3,2,1", "25,8,2,1,1", "33,4,2,2,1", "33,8,2,1,1",
+                                  "9,4,3,4,2", "17,8,3,2,2", "17,8,4,1,2", "17,8,2,3,2", "17,4,4,3,2",
+                                  "25,4,3,2,2", "33,4,3,2,2", "15,8,3,2,2", "17,16,2,1,2"])
 def test_all_pass_geometries(h1, geom, monkeypatch):
     monkeypatch.setenv("HEAT1D_GEOM", geom)
     N, nt = 300_001, 29

@@ -1,0 +1,7 @@
+set -x
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q -k "geometries or ragged or c1_ or cross_T or virtual" > gpurun_out/pytest_e.log 2>&1; echo pytest=$?
+timeout 900 python tools/sweep.py --nt 1200 --geoms 17,8,3,2,0 17,8,3,2,1 33,4,3,2,0 25,4,3,2,0 17,4,3,4,0 15,8,3,2,0 --T 8 10 12 14 16 --k 0.4 0.5 > gpurun_out/sweep4.jsonl 2> gpurun_out/sweep4.err; echo sweep=$?
+CMD="python tools/sweep.py --N 67108864 --nt 24 --T 12 --k 0.4 0.5 --reps 1 --geoms 17,8,3,2,0 17,8,3,2,1"
+$CMD > gpurun_out/ncu_plain3.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k2 -s 2 -c 8 -o gpurun_out/k2_v2_T12 $CMD > gpurun_out/ncu_run3.log 2>&1; echo ncu=$?
