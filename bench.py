@@ -314,7 +314,10 @@ def main():
         except Exception:
             pass
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "peak_kind": peak_kind, "kernel": "k2_pass", "launches": k2_launches,
+                "traffic": traffic, "peak_kind": peak_kind,
+                "kernel": ["k2_pass", "k2w_pass", "k2p_pass"][info["pass_kind"]] + "<V=%d,NW=%d,S=%d,OPS=%d>" % (
+                    info["pass_V"], info["pass_NW"], info["pass_S"], info["dp_ops"]),
+                "launches": k2_launches,
                 "avg_launch_ms": avg_ms, "alg_bytes_per_launch": alg_bytes,
                 "glups_roofline": min(hbm / (16.0 / T), 9306.0) * world,
                 "glups_frac_of_roofline": value / (min(hbm / (16.0 / T), 9306.0) * world),

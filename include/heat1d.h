@@ -107,6 +107,8 @@ typedef struct {
     int64_t pad;            /* ghost cells allocated on each side of a slab                 */
     int32_t tile_cells;     /* output cells per CTA tile of the pass kernel (at T)          */
     int32_t grid;           /* CTAs per pass-kernel launch (persistent)                     */
+    int32_t pass_kind;      /* pass-kernel variant: 0 CTA tiles, 1 warp spans, 2 producer warp */
+    int32_t pass_V, pass_NW, pass_S; /* cells/lane, compute warps/CTA, TMA stages            */
 } heat1d_info_t;
 
 /* Exchange plan of one rank (pure host logic; usable without a GPU).  Offsets

@@ -643,6 +643,10 @@ int heat1d_info(heat1d_t h, heat1d_info_t *info) {
     info->pad = h->pad;
     info->tile_cells = (int32_t)h->geom.tile_out(h->T);
     info->grid = h->last_grid;
+    info->pass_kind = h->geom.kind;
+    info->pass_V = h->geom.V;
+    info->pass_NW = h->geom.NW;
+    info->pass_S = h->geom.S;
     return HEAT1D_OK;
 }
 

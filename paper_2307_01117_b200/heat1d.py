@@ -76,6 +76,10 @@ class Info(ctypes.Structure):
         ("pad", ctypes.c_int64),
         ("tile_cells", ctypes.c_int32),
         ("grid", ctypes.c_int32),
+        ("pass_kind", ctypes.c_int32),
+        ("pass_V", ctypes.c_int32),
+        ("pass_NW", ctypes.c_int32),
+        ("pass_S", ctypes.c_int32),
     ]
 
 
