@@ -87,6 +87,9 @@ typedef struct {
     int32_t blocking;       /* nonzero (default): heat1d_run returns after the device is done;
                                zero: heat1d_run only enqueues on `stream`                   */
     int32_t use_graphs;     /* nonzero (default): replay pass sequences as CUDA graphs      */
+    int32_t resident;       /* -1 (default) auto, 0 never, 1 required: solve a ring that fits
+                               on chip (single slab, single rank, <= ~1.8 M cells) in ONE
+                               cooperative launch with the slab held in registers (K6)      */
     void *stream;           /* cudaStream_t for compute (e.g. torch's current stream);
                                NULL = a stream owned by the handle                          */
     void *comm_stream;      /* cudaStream_t for halo exchange; NULL = owned by the handle   */
@@ -109,6 +112,8 @@ typedef struct {
     int32_t grid;           /* CTAs per pass-kernel launch (persistent)                     */
     int32_t pass_kind;      /* pass-kernel variant: 0 CTA tiles, 1 warp spans, 2 producer warp */
     int32_t pass_V, pass_NW, pass_S; /* cells/lane, compute warps/CTA, TMA stages            */
+    int32_t resident;       /* 1 if runs use the register-resident kernel K6                */
+    int32_t resident_warps; /* warps of the last K6 launch                                  */
 } heat1d_info_t;
 
 /* Exchange plan of one rank (pure host logic; usable without a GPU).  Offsets

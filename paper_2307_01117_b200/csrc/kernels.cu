@@ -98,7 +98,7 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     return p;
 }
 
-constexpr unsigned FULL = 0xffffffffu;
+
 
 }  // namespace
 
@@ -154,7 +154,7 @@ k2_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, 
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    const int warp = tid >> 5;
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform for the compiler
     const int OW = 32 * V - 2 * T;
     const int64_t W = (int64_t)NW * OW;
 
@@ -257,7 +257,7 @@ k2w_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int BAR_BYTES = ((NW * S * 8 + 127) / 128) * 128;
     const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
+    const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);  // warp-uniform for the compiler
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw) + warp * S;
     double *slots = reinterpret_cast<double *>(smem_raw + BAR_BYTES) + (size_t)warp * S * slot_doubles;
 
@@ -362,7 +362,7 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    const int warp = tid >> 5;
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform for the compiler
     const int OW = 32 * V - 2 * T;
     const int64_t W = (int64_t)NW * OW;
     const int64_t stride = gridDim.x;
@@ -498,10 +498,11 @@ PassFn lookup_pass(int V, int NW, int S, int ops, int kind) {
 }  // namespace
 
 PassGeom choose_geom(int64_t n_out, int T, int num_sms) {
-    // Default: CTA tiles of 8 compute warps x V=17 cells/lane plus
-    // a TMA producer warp, 3 stages (~100 KB), 2 CTAs per SM.  Rings too small
-    // to give every CTA a tile use 4-warp tiles of V=9.
-    PassGeom g{17, 8, 3, 2, 2};
+    // Default (profiles/r01_sweeps.jsonl): CTA tiles of 4 compute
+    // warps x V=33 cells/lane plus a TMA producer warp, 3 stages (~102 KB),
+    // 2 CTAs per SM.  Rings too small to give every CTA a tile use 4-warp
+    // tiles of V=9.
+    PassGeom g{33, 4, 3, 2, 2};
     if (n_out < (int64_t)num_sms * g.ctas_per_sm * g.tile_out(T)) g = PassGeom{9, 4, 3, 4, 2};
     return g;
 }

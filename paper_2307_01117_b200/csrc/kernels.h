@@ -49,4 +49,11 @@ cudaError_t launch_wrap_fill(double *A, int64_t n, int64_t pad, cudaStream_t st)
 cudaError_t launch_init_uniform(double *u, int64_t count, int64_t first, uint64_t seed,
                                 double lo, double hi, cudaStream_t st);
 
+// K6: whole nt-step solve of a single-slab ring held in registers (resident.cu).
+int64_t resident_capacity(int T, int num_sms);
+bool resident_fits(int ops, int64_t n, int T, int num_sms);  // plan + co-residency check
+size_t resident_scratch_bytes(int T, int num_sms);
+cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double r,
+                            void *scratch, int num_sms, cudaStream_t st, int *warps_out);
+
 }  // namespace heat1d

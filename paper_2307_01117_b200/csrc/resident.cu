@@ -1,0 +1,351 @@
+// resident.cu -- K6: register-resident ring for slabs that fit on chip.
+//
+// A ring of up to ~2 M cells (C1, C2, C5 of BASELINE.json) is latency-bound
+// on B200 if every T steps costs a kernel launch.  K6 runs the WHOLE nt-step
+// solve in one cooperative launch.  The slab is cut into Ns equal "spans";
+// each span keeps its owned cells plus a T-deep halo on each side in
+// registers (V cells per lane, the per-warp trapezoid of K2), advances T
+// steps, publishes its first and last T owned cells to a global edge buffer
+// and refreshes its halos from its two neighbour spans' edges -- the paper's
+// ghost-zone exchange between segments at depth T, between warps.
+//
+// Synchronisation is pairwise: per-span release/acquire flags in global
+// memory, no grid-wide barrier.  A warp owns SPW = 2 spans half a ring apart
+// and alternates between them (compute A, publish A, refresh B, compute B,
+// publish B, refresh A, ...), so each span's halo exchange is in flight while
+// the warp computes its other span.  Edge buffers are double-buffered by
+// period parity: a span writes period p+2 edges only after its neighbours
+// published p+1, i.e. after they finished reading period p.
+#include <cstdint>
+#include <cstdlib>
+
+#include "kernels.h"
+#include "stencil.cuh"
+
+namespace heat1d {
+
+namespace {
+
+__device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <int V, int OPS, bool EARLY>
+__device__ __forceinline__ void step_regs(const double (&u)[V], double (&v)[V], double &L, double &R,
+                                          double r) {
+    if constexpr (EARLY) {
+        v[0] = eq2<OPS>(L, u[0], u[1], r);
+        v[V - 1] = eq2<OPS>(u[V - 2], u[V - 1], R, r);
+        L = __shfl_up_sync(0xffffffffu, v[V - 1], 1);
+        R = __shfl_down_sync(0xffffffffu, v[0], 1);
+#pragma unroll
+        for (int j = 1; j < V - 1; ++j) v[j] = eq2<OPS>(u[j - 1], u[j], u[j + 1], r);
+    } else {
+        L = __shfl_up_sync(0xffffffffu, u[V - 1], 1);
+        R = __shfl_down_sync(0xffffffffu, u[0], 1);
+#pragma unroll
+        for (int j = 1; j < V - 1; ++j) v[j] = eq2<OPS>(u[j - 1], u[j], u[j + 1], r);
+        v[0] = eq2<OPS>(L, u[0], u[1], r);
+        v[V - 1] = eq2<OPS>(u[V - 2], u[V - 1], R, r);
+    }
+}
+
+// Tp steps on u (v is scratch), result in u.
+template <int V, int OPS, bool EARLY>
+__device__ __forceinline__ void steps_regs(double (&u)[V], double (&v)[V], int Tp, double r) {
+    double L = 0.0, R = 0.0;
+    if constexpr (EARLY) {
+        L = __shfl_up_sync(0xffffffffu, u[V - 1], 1);
+        R = __shfl_down_sync(0xffffffffu, u[0], 1);
+    }
+    int s = 0;
+    for (; s + 2 <= Tp; s += 2) {
+        step_regs<V, OPS, EARLY>(u, v, L, R, r);
+        step_regs<V, OPS, EARLY>(v, u, L, R, r);
+    }
+    if (s < Tp) {
+        step_regs<V, OPS, EARLY>(u, v, L, R, r);
+#pragma unroll
+        for (int j = 0; j < V; ++j) u[j] = v[j];
+    }
+}
+
+// One span: its cells [start, start+own) of the ring, staged in `row`
+// (positions 0..T-1 left halo, T..T+own-1 owned, then right halo).
+struct Span {
+    int64_t start;
+    int own, id, left, right;
+    double *row;
+};
+
+__device__ __forceinline__ Span make_span(int id, int Ns, int64_t n, double *row) {
+    const int64_t base = n / Ns, rem = n % Ns;
+    Span s;
+    s.id = id;
+    s.own = (int)(base + (id < rem ? 1 : 0));
+    s.start = (int64_t)id * base + (id < rem ? id : rem);
+    s.left = (id + Ns - 1) % Ns;
+    s.right = (id + 1) % Ns;
+    s.row = row;
+    return s;
+}
+
+template <int V>
+__device__ __forceinline__ void load_span(const Span &s, const double *__restrict__ A, int64_t n, int T,
+                                          int lane) {
+    const int span = s.own + 2 * T;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {  // uniform trip count (no divergent loop before the shuffles)
+        const int p = lane + 32 * k;
+        double x = 0.0;
+        if (p < span) {
+            int64_t g = (s.start - T + p) % n;  // rings shorter than a halo wrap more than once
+            if (g < 0) g += n;
+            x = A[g];
+        }
+        s.row[p] = x;
+    }
+    __syncwarp();
+}
+
+template <int V>
+__device__ __forceinline__ void row_to_regs(const double *row, double (&u)[V], int lane) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) u[j] = row[lane * V + j];
+}
+
+template <int V>
+__device__ __forceinline__ void regs_to_row(const double (&u)[V], double *row, int lane) {
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < V; ++j) row[lane * V + j] = u[j];
+    __syncwarp();
+}
+
+// edges: [Ns][2 parities][2 sides][T]; publish this span's period-p edges
+__device__ __forceinline__ void publish(const Span &s, int T, unsigned p, double *edges, unsigned *flags,
+                                        int lane) {
+    double *E = edges + ((size_t)s.id * 4 + (p & 1) * 2) * T;
+    if (lane < T) {                         // T <= 32
+        E[lane] = s.row[T + lane];          // side 0: first T owned cells
+        E[T + lane] = s.row[s.own + lane];  // side 1: last T owned cells
+    }
+    __syncwarp();  // orders the lanes' writes before lane 0's (cumulative) release
+    if (lane == 0) st_release(flags + s.id, p + 1);
+}
+
+// wait for the neighbours' period-p edges and write them into the halos
+__device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, const double *edges,
+                                        const unsigned *flags, int lane) {
+    // every lane polls (one coalesced request per poll); the vote makes the exit
+    // warp-uniform, so ptxas keeps the step loop's shuffles non-collective.
+    // Relaxed polls: an acquire at gpu scope invalidates L1 (CCTL.IVALL) each
+    // time; one acquire per flag after the wait orders the edge reads.
+    while (!__all_sync(0xffffffffu, ld_relaxed(flags + s.left) >= p + 1 && ld_relaxed(flags + s.right) >= p + 1)) {
+    }
+    (void)ld_acquire(flags + s.left);
+    (void)ld_acquire(flags + s.right);
+    __syncwarp();
+    const double *LE = edges + ((size_t)s.left * 4 + (p & 1) * 2) * T + T;  // left's side 1
+    const double *RE = edges + ((size_t)s.right * 4 + (p & 1) * 2) * T;     // right's side 0
+    if (lane < T) {
+        s.row[lane] = __ldcg(LE + lane);
+        s.row[s.own + T + lane] = __ldcg(RE + lane);
+    }
+    __syncwarp();
+}
+
+}  // namespace
+
+template <int V, int OPS, int SPW, bool EARLY>
+__global__ void __launch_bounds__(256)
+k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t nt, double r,
+            double *__restrict__ edges, unsigned *__restrict__ flags, int Wt) {
+    extern __shared__ __align__(16) double srow[];
+    const int lane = threadIdx.x & 31;
+    const int wib = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);  // warp-uniform for the compiler
+    const int gw = blockIdx.x * (blockDim.x >> 5) + wib;
+    if (gw >= Wt) return;  // whole warps only; no CTA-wide barrier is used below
+    const int Ns = SPW * Wt;
+    double *rows = srow + (size_t)wib * SPW * (32 * V + 1);
+    const Span a = make_span(gw, Ns, n, rows);
+    double ua[V], v[V];
+    load_span<V>(a, A, n, T, lane);
+    row_to_regs<V>(a.row, ua, lane);
+
+    if constexpr (SPW == 1) {
+        int64_t done = 0;
+        for (unsigned p = 0;; ++p) {
+            const int Tp = (int)((nt - done) < T ? (nt - done) : T);
+            steps_regs<V, OPS, EARLY>(ua, v, Tp, r);
+            regs_to_row<V>(ua, a.row, lane);
+            done += Tp;
+            if (done >= nt) break;
+            publish(a, T, p, edges, flags, lane);
+            refresh(a, T, p, edges, flags, lane);
+            row_to_regs<V>(a.row, ua, lane);
+        }
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            const int q = T + lane + 32 * k;
+            if (q < T + a.own) B[a.start + (q - T)] = a.row[q];
+        }
+    } else {
+        const Span b = make_span(gw + Wt, Ns, n, rows + (32 * V + 1));
+        double ub[V];
+        load_span<V>(b, A, n, T, lane);
+        row_to_regs<V>(b.row, ub, lane);
+        int64_t done = 0;
+        for (unsigned p = 0;; ++p) {
+            const int Tp = (int)((nt - done) < T ? (nt - done) : T);
+            const bool last = done + Tp >= nt;
+            steps_regs<V, OPS, EARLY>(ua, v, Tp, r);  // A: halos valid for period p
+            regs_to_row<V>(ua, a.row, lane);
+            if (!last) publish(a, T, p, edges, flags, lane);
+            if (p > 0) {  // B's halos for period p: neighbours' period p-1 edges
+                refresh(b, T, p - 1, edges, flags, lane);
+                row_to_regs<V>(b.row, ub, lane);
+            }
+            steps_regs<V, OPS, EARLY>(ub, v, Tp, r);
+            regs_to_row<V>(ub, b.row, lane);
+            if (!last) publish(b, T, p, edges, flags, lane);
+            done += Tp;
+            if (last) break;
+            refresh(a, T, p, edges, flags, lane);  // overlapped with B's compute above
+            row_to_regs<V>(a.row, ua, lane);
+        }
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            const int q = T + lane + 32 * k;
+            if (q < T + a.own) B[a.start + (q - T)] = a.row[q];
+            if (q < T + b.own) B[b.start + (q - T)] = b.row[q];
+        }
+    }
+}
+
+namespace {
+constexpr int RV = 17;        // cells per lane
+// warps per SM the register budget allows: ~100 regs (1 span/warp), ~156 (2 spans/warp)
+constexpr int MAX_WPS1 = 20, MAX_WPS2 = 12;
+constexpr int MAX_WPS = MAX_WPS1;
+
+struct ResPlan {
+    int64_t wt = 0, nw = 0, grid = 0;
+    int spw = 2;
+    size_t smem = 0;
+};
+
+int res_early() {
+    const char *e = getenv("HEAT1D_K6_EARLY");  // tuning knob
+    return e ? atoi(e) : 1;
+}
+
+const void *res_fn(int ops, int spw) {
+    const bool early = res_early() != 0;
+#define RF(o, s, e) (const void *)&k6_resident<RV, o, s, e>
+    if (spw == 1) return early ? (ops == 4 ? RF(4, 1, true) : RF(3, 1, true)) : (ops == 4 ? RF(4, 1, false) : RF(3, 1, false));
+    return early ? (ops == 4 ? RF(4, 2, true) : RF(3, 2, true)) : (ops == 4 ? RF(4, 2, false) : RF(3, 2, false));
+#undef RF
+}
+
+cudaError_t res_attr(const void *fn) {
+    static const void *done[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    for (const void *d : done)
+        if (d == fn) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         2 * 16 * (32 * RV + 1) * 8);
+    if (e != cudaSuccess) return e;
+    for (auto &d : done)
+        if (!d) {
+            d = fn;
+            break;
+        }
+    return cudaSuccess;
+}
+
+// Split the ring into Ns = spw*Wt equal spans (each owning >= T cells, span
+// own + 2T <= 32*RV) with warps balanced across SMs.
+bool res_plan(int ops, int64_t n, int T, int num_sms, ResPlan *p) {
+    const int cap = 32 * RV - 2 * T;
+    if (T < 1 || cap <= 0 || n < T) return false;
+    // 1 span per warp by default (profiles/r01_k6_ab_*.jsonl: 2 spans per warp do
+    // not pay on B200); HEAT1D_K6_SPW=2 selects the alternating two-span warps.
+    p->spw = 1;
+    if (const char *e = getenv("HEAT1D_K6_SPW")) p->spw = (atoi(e) == 2 && n >= 2 * (int64_t)T) ? 2 : 1;
+    const int64_t ns_min = (n + cap - 1) / cap;
+    const int64_t wt_min = (ns_min + p->spw - 1) / p->spw;
+    if (wt_min <= num_sms) {
+        p->wt = wt_min;  // one warp per CTA, each on its own SM
+        p->nw = 1;
+        p->grid = p->wt;
+    } else {
+        const int64_t wps = (wt_min + num_sms - 1) / num_sms;
+        if (wps > (p->spw == 1 ? MAX_WPS1 : MAX_WPS2)) return false;
+        const int64_t cps = wps > (p->spw == 1 ? 10 : 6) ? 2 : 1;
+        p->nw = (wps + cps - 1) / cps;
+        p->grid = (int64_t)num_sms * cps;
+        p->wt = p->grid * p->nw;
+    }
+    while (p->wt > 1 && n / (p->wt * p->spw) < T) {
+        p->wt = (p->wt + 1) / 2;
+        p->nw = 1;
+        p->grid = p->wt;
+    }
+    const int64_t ns = p->wt * p->spw;
+    if (n / ns < T || n / ns + (n % ns ? 1 : 0) + 2 * T > 32 * RV) return false;
+    p->smem = (size_t)p->nw * p->spw * (32 * RV + 1) * sizeof(double);
+    const void *fn = res_fn(ops, p->spw);
+    if (res_attr(fn) != cudaSuccess) return false;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, (int)(p->nw * 32), p->smem) != cudaSuccess)
+        return false;
+    return (int64_t)occ * num_sms >= p->grid;  // cooperative launch: all CTAs co-resident
+}
+
+}  // namespace
+
+int64_t resident_capacity(int T, int num_sms) {
+    const int64_t a = (int64_t)MAX_WPS1, b = 2 * (int64_t)MAX_WPS2;
+    return (int64_t)num_sms * (a > b ? a : b) * (32 * RV - 2 * T);
+}
+
+bool resident_fits(int ops, int64_t n, int T, int num_sms) {
+    ResPlan p;
+    return res_plan(ops, n, T, num_sms, &p);
+}
+
+size_t resident_scratch_bytes(int T, int num_sms) {
+    const int64_t ns = (int64_t)num_sms * (MAX_WPS1 > 2 * MAX_WPS2 ? MAX_WPS1 : 2 * MAX_WPS2);
+    return (size_t)ns * 4 * T * sizeof(double) + (size_t)ns * sizeof(unsigned) + 256;
+}
+
+cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double r,
+                            void *scratch, int num_sms, cudaStream_t st, int *warps_out) {
+    ResPlan p;
+    if (!res_plan(ops, n, T, num_sms, &p)) return cudaErrorInvalidValue;
+    const int64_t ns = p.wt * p.spw;
+    double *edges = static_cast<double *>(scratch);
+    unsigned *flags = reinterpret_cast<unsigned *>(edges + (size_t)ns * 4 * T);
+    cudaError_t e = cudaMemsetAsync(flags, 0, (size_t)ns * sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+    int Wt = (int)p.wt;
+    void *args[] = {(void *)&A, (void *)&B, (void *)&n, (void *)&T, (void *)&nt, (void *)&r, (void *)&edges,
+                    (void *)&flags, (void *)&Wt};
+    if (warps_out) *warps_out = Wt;
+    return cudaLaunchCooperativeKernel(res_fn(ops, p.spw), dim3((unsigned)p.grid), dim3((unsigned)(p.nw * 32)),
+                                       args, p.smem, st);
+}
+
+}  // namespace heat1d

@@ -50,6 +50,7 @@ class Opts(ctypes.Structure):
         ("kernel", ctypes.c_int32),
         ("blocking", ctypes.c_int32),
         ("use_graphs", ctypes.c_int32),
+        ("resident", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
         ("comm_stream", ctypes.c_void_p),
     ]
@@ -80,6 +81,8 @@ class Info(ctypes.Structure):
         ("pass_V", ctypes.c_int32),
         ("pass_NW", ctypes.c_int32),
         ("pass_S", ctypes.c_int32),
+        ("resident", ctypes.c_int32),
+        ("resident_warps", ctypes.c_int32),
     ]
 
 
@@ -216,7 +219,7 @@ class Heat1D:
                  mode: str = "matched", denominator: str = "dx2", allow_unstable: bool = False,
                  rank: int = 0, nranks: int = 1, nccl_id: Optional[bytes] = None, virtual_slabs: int = 1,
                  kernel: str = "auto", device: int = -1, stream=None, comm_stream=None,
-                 blocking: bool = True, use_graphs: bool = True):
+                 blocking: bool = True, use_graphs: bool = True, resident: Optional[bool] = None):
         self._lib = load()
         o = default_opts()
         o.device = device
@@ -233,6 +236,7 @@ class Heat1D:
         o.kernel = KERNELS[kernel]
         o.blocking = 1 if blocking else 0
         o.use_graphs = 1 if use_graphs else 0
+        o.resident = -1 if resident is None else (1 if resident else 0)
         o.stream = _stream_ptr(stream)
         o.comm_stream = _stream_ptr(comm_stream)
         h = ctypes.c_void_p()

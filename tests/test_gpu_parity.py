@@ -77,11 +77,51 @@ def test_zero_diffusivity_identity(h1):
 @pytest.mark.parametrize("N", [4097, 100_003, (1 << 20) + 7])
 @pytest.mark.parametrize("T", [1, 3, 8, 12])
 @pytest.mark.parametrize("k", [0.4, 0.5])
-def test_ragged_multi_tile(h1, N, T, k):
+@pytest.mark.parametrize("resident", [False, None])
+def test_ragged_multi_tile(h1, N, T, k, resident):
+    """K2 passes (resident=False) and the auto choice (K6 for these on-chip rings)."""
     nt = 2 * T + 3           # full passes + a tail pass
     u0 = synth.uniform(N + T, 0, N, -1.0, 1.0)
     want = oracle.run(u0, k, nt)
-    assert_bitwise(gpu_run(h1, u0, N, 1, nt, k, T=T), want, "N=%d T=%d" % (N, T))
+    assert_bitwise(gpu_run(h1, u0, N, 1, nt, k, T=T, resident=resident), want, "N=%d T=%d" % (N, T))
+
+
+@pytest.mark.parametrize("N", [1, 2, 7, 33, 544, 545, 5000, 80_000, 1_000_000, 1_400_000])
+@pytest.mark.parametrize("T", [1, 5, 16, 32])
+def test_resident_kernel(h1, N, T):
+    """K6 (whole solve in one cooperative launch, slab in registers) vs the oracle:
+    one warp, a few warps, one warp per SM, many warps per SM, near capacity."""
+    nt = 3 * T + 2
+    u0 = synth.uniform(N + 7 * T, 0, N, -1.0, 1.0)
+    want = oracle.run(u0, 0.4, nt)
+    with h1.Heat1D(N, 1, nt, 0.4, 1.0, 1.0, T=T, resident=True) as h:
+        assert h.info()["resident"] == 1
+        h.set_initial(u0)
+        h.run(nt)
+        got = h.get()
+        h.run(1)                          # a second run continues from the state
+        assert_bitwise(h.get(), oracle.run(want, 0.4, 1), "K6 N=%d continue" % N)
+    assert_bitwise(got, want, "K6 N=%d T=%d" % (N, T))
+
+
+@pytest.mark.parametrize("early", ["0", "1"])
+def test_resident_two_span_warps(h1, monkeypatch, early):
+    """K6 variants behind tuning knobs: two spans per warp, early shuffles."""
+    monkeypatch.setenv("HEAT1D_K6_SPW", "2")
+    monkeypatch.setenv("HEAT1D_K6_EARLY", early)
+    for N, T in [(40, 8), (100_003, 32), (1 << 20, 16)]:
+        nt = 2 * T + 5
+        u0 = synth.uniform(N, 0, N, -1.0, 1.0)
+        with h1.Heat1D(N, 1, nt, 0.5, 1.0, 1.0, T=T, resident=True) as h:
+            h.set_initial(u0)
+            h.run()
+            assert_bitwise(h.get(), oracle.run(u0, 0.5, nt), "K6 spw=2 N=%d" % N)
+
+
+def test_resident_refuses_too_large(h1):
+    with pytest.raises(h1.Heat1DError) as ei:
+        h1.Heat1D(1 << 24, 1, 10, 0.5, 1.0, 1.0, resident=True)
+    assert ei.value.status == 7
 
 
 @pytest.mark.parametrize("geom", ["9,4,3,4,0", "9,8,4,2,0", "17,4,4,2,0", "17,8,2,1,0", "17,8,3,2,0",
@@ -96,7 +136,7 @@ def test_all_pass_geometries(h1, geom, monkeypatch):
     u0 = synth.uniform(77, 0, N, -1.0, 1.0)
     for k, T in [(0.4, 7), (0.5, 12)]:
         want = oracle.run(u0, k, nt)
-        assert_bitwise(gpu_run(h1, u0, N, 1, nt, k, T=T), want, "geom %s T=%d" % (geom, T))
+        assert_bitwise(gpu_run(h1, u0, N, 1, nt, k, T=T, resident=False), want, "geom %s T=%d" % (geom, T))
 
 
 # ------------------------------------------------------------------ C2 (paper's workload size)
@@ -125,7 +165,8 @@ def test_cross_T_bitwise(h1):
     u0 = synth.uniform(5, 0, N, -1.0, 1.0)
     ref = gpu_run(h1, u0, N, 1, nt, 0.4, kernel="naive")
     for T in [1, 2, 3, 4, 6, 8, 11, 12, 16, 24, 32]:
-        assert_bitwise(gpu_run(h1, u0, N, 1, nt, 0.4, T=T), ref, "T=%d" % T)
+        for res in (False, True):
+            assert_bitwise(gpu_run(h1, u0, N, 1, nt, 0.4, T=T, resident=res), ref, "T=%d res=%s" % (T, res))
 
 
 def test_split_run_invariance(h1):
