@@ -29,6 +29,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "fp64 cell-updates/sec (GLUPS) at 1/2/4/8 B200 and % of HBM/FP64 roofline"
 FALLBACK_HBM_GBS = 6650.0
+SMS, FP64_LANES, SM_MHZ_MAX = 148, 64, 1965.0             # B200: fp64 lanes per SM, max SM clock
+FP64_TFLOPS = SMS * FP64_LANES * 2 * SM_MHZ_MAX * 1e6 / 1e12  # 37.2 TFLOP/s (FMA = 2 flop)
 
 
 def parse():
@@ -301,27 +303,42 @@ def main():
     T = info["T"]
     roof = None
     if k2_launches:
+        # dominant kernel: K2 (one T-step pass per launch) or K6 (the whole solve per launch)
         avg_ms = k2_ms / k2_launches
-        n_out = count if world == 1 else count - 2 * T
-        alg_bytes = 16.0 * n_out          # 8 B read + 8 B written per cell per pass (halo re-reads excluded)
-        achieved = alg_bytes / (avg_ms / 1e3) / 1e9
+        upd_launch = count * cfg.nt * args.steps / k2_launches   # cell updates per launch, this rank
+        steps_per_pass = cfg.nt if info["resident"] else T        # steps per HBM round trip of the state
+        alg_bytes = 16.0 * count * (upd_launch / count) / steps_per_pass  # 8 B read + 8 B written per cell per pass
+        hbm_term = hbm / (16.0 / steps_per_pass)                 # GLUPS bound by HBM (BASELINE.json)
+        fp64_term = FP64_TFLOPS * 1e3 / 4.0                      # GLUPS bound by FP64 peak / 4 flop
+        bj_roof = min(hbm_term, fp64_term) * world
+        kernel = ("k6_resident<V=17>" if info["resident"] else
+                  ["k2_pass", "k2w_pass", "k2p_pass"][info["pass_kind"]] + "<V=%d,NW=%d,S=%d>" % (
+                      info["pass_V"], info["pass_NW"], info["pass_S"])) + "<OPS=%d>" % info["dp_ops"]
+        if hbm_term < fp64_term:
+            achieved = alg_bytes / (avg_ms / 1e3) / 1e9
+            roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                    "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes}
+        else:
+            # fp64-pipe bound: algorithmic fp64 instructions (dp_ops per update) per second against the
+            # pipe's issue rate 148 SM x 64 lanes x 1.965 GHz
+            dpi = info["dp_ops"] * upd_launch / (avg_ms / 1e3) / 1e12
+            peak = SMS * FP64_LANES * SM_MHZ_MAX * 1e6 / 1e12
+            roof = {"bound": "alu", "achieved": dpi, "peak": peak, "unit": "Tinst/s (fp64 DFMA/DADD/DMUL)",
+                    "frac": dpi / peak, "peak_kind": "derived: 148 SM x 64 fp64 lanes x 1.965 GHz",
+                    "alg_fp64_inst_per_launch": info["dp_ops"] * upd_launch, "alg_bytes_per_launch": alg_bytes}
         traffic = None
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-                tr = json.load(f)
-            key = "%s_T%d_%s" % (cfg.name, T, args.mode)
-            traffic = tr.get(key)
+                traffic = json.load(f).get("%s_T%d_%s" % (cfg.name, T, args.mode))
         except Exception:
             pass
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "peak_kind": peak_kind,
-                "kernel": ["k2_pass", "k2w_pass", "k2p_pass"][info["pass_kind"]] + "<V=%d,NW=%d,S=%d,OPS=%d>" % (
-                    info["pass_V"], info["pass_NW"], info["pass_S"], info["dp_ops"]),
-                "launches": k2_launches,
-                "avg_launch_ms": avg_ms, "alg_bytes_per_launch": alg_bytes,
-                "glups_roofline": min(hbm / (16.0 / T), 9306.0) * world,
-                "glups_frac_of_roofline": value / (min(hbm / (16.0 / T), 9306.0) * world),
-                "k2_share_of_step": k2_ms / ms if world == 1 else None}
+        roof.update({
+            "traffic": traffic, "kernel": kernel, "launches": k2_launches, "avg_launch_ms": avg_ms,
+            "steps_per_launch": upd_launch / count,
+            "baseline_json_roofline_glups": bj_roof,
+            "baseline_json_frac": value / bj_roof,
+            "baseline_json_bound": "hbm" if hbm_term < fp64_term else "fp64 (37.2 TFLOP/s / 4 flop)",
+            "kernel_share_of_step": k2_ms / ms if world == 1 else None})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -96,6 +96,7 @@ int set_error(heat1d_t h, int status, const char *fmt, ...) {
 
 int fail_cuda(heat1d_t h, cudaError_t e, const char *what, int line) {
     if (h) h->poisoned = HEAT1D_ECUDA;
+    cudaGetLastError();  // clear a non-sticky error so it does not leak into other handles
     return set_error(h, HEAT1D_ECUDA, "CUDA error %s (%s) at heat1d.cpp:%d: %s", cudaGetErrorName(e),
                      cudaGetErrorString(e), line, what);
 }
@@ -157,10 +158,12 @@ int64_t min_slab(int64_t nx, int64_t np, int32_t G) {
 }
 
 int auto_T(int ops) {
-    // the largest T whose sustained (power-capped) throughput stays
-    // >= 70% of the HBM roofline 409*T GLUPS: 10 for the 4-op arithmetic
-    // (general r), 12 for the 3-op one (r a power of two, or fast mode).
-    return ops == 4 ? 10 : 12;
+    // DESIGN.md §6 (T sweeps in profiles/): throughput rises with T up to the
+    // largest halo the kernels support, because each pass moves 16/T bytes per
+    // update and the freed HBM power lets the SM clock rise under the 1 kW cap;
+    // past T ~ 12 (4-op) / 16 (3-op) the pass is fp64-issue bound.
+    (void)ops;
+    return HEAT1D_T_MAX;
 }
 
 bool parse_geom_env(PassGeom *g) {
@@ -475,15 +478,6 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     h->use_graphs = o.use_graphs != 0;
     h->ops = (o.mode == HEAT1D_MODE_FAST || is_pow2(r) || r == 0.0) ? 3 : 4;
     // r == 0: fma(0, t, b) == b + 0*t == b for finite t (identity either way)
-    int T = o.T > 0 ? o.T : auto_T(h->ops);
-    if (o.kernel == HEAT1D_KERNEL_NAIVE) T = 1;
-    // K6 candidate: one slab on one rank, pass kernel, fits on chip (checked below)
-    const bool res_ok = (G == 1 && o.kernel == HEAT1D_KERNEL_AUTO && o.resident != 0);
-    if (res_ok && o.T == 0) T = 32;  // K6 period (halo refresh every 32 steps)
-    if (T > mslab) T = (int)mslab;  // a slab must hold its own halo (DESIGN.md §5)
-    h->T = T;
-    h->pad = pad_for(T);
-
     auto bail = [&](int rc) {
         heat1d_destroy(h);
         return rc;
@@ -502,6 +496,38 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
         return set_error(nullptr, HEAT1D_ECUDA, "no CUDA device");
     }
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
+
+    // T and the kernel family.  K6 (whole solve on chip) for one slab on one rank
+    // when the ring fits; otherwise K2 passes.
+    int T = o.T > 0 ? o.T : auto_T(h->ops);
+    if (o.kernel == HEAT1D_KERNEL_NAIVE) T = 1;
+    if (T > mslab) T = (int)mslab;  // a slab must hold its own halo (DESIGN.md §5)
+    const bool res_ok = (G == 1 && o.kernel == HEAT1D_KERNEL_AUTO && o.resident != 0);
+    if (res_ok) {
+        const int64_t n0 = h->N;
+        int Tr = o.T > 0 ? o.T : 32;  // K6 period: halo refresh every 32 steps
+        if (Tr > n0) Tr = (int)n0;
+        int coop = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
+        const bool fits = coop && n0 <= heat1d::resident_capacity(Tr, h->num_sms) && n0 >= Tr &&
+                          heat1d::resident_fits(h->ops, n0, Tr, h->num_sms);
+        cudaGetLastError();
+        if (fits) {
+            h->resident = true;
+            T = Tr;
+        } else if (o.resident == 1) {
+            set_error(nullptr, HEAT1D_EUNSUPPORTED, "ring of %lld cells does not fit the resident kernel",
+                      (long long)n0);
+            delete h;
+            return HEAT1D_EUNSUPPORTED;
+        }
+    } else if (o.resident == 1) {
+        set_error(nullptr, HEAT1D_EUNSUPPORTED, "resident kernel needs one slab on one rank");
+        delete h;
+        return HEAT1D_EUNSUPPORTED;
+    }
+    h->T = T;
+    h->pad = pad_for(T);
 
     // slabs
     const int ns = o.virtual_slabs;
@@ -567,27 +593,12 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
         }
     }
     if (!parse_geom_env(&h->geom)) h->geom = heat1d::choose_geom(h->slabs[0].count, h->T, h->num_sms);
-    if (res_ok) {
-        const int64_t n0 = h->slabs[0].count;
-        const bool fits = n0 <= heat1d::resident_capacity(h->T, h->num_sms) && n0 >= h->T &&
-                          heat1d::resident_fits(h->ops, n0, h->T, h->num_sms);
-        int coop = 0;
-        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
-        if (fits && coop) {
-            if (cudaMalloc(&h->res_scratch, heat1d::resident_scratch_bytes(h->T, h->num_sms)) != cudaSuccess) {
-                cudaGetLastError();
-                set_error(nullptr, HEAT1D_ENOMEM, "resident scratch");
-                return bail(HEAT1D_ENOMEM);
-            }
-            h->resident = true;
-        } else if (o.resident == 1) {
-            set_error(nullptr, HEAT1D_EUNSUPPORTED, "ring of %lld cells does not fit the resident kernel",
-                      (long long)n0);
-            return bail(HEAT1D_EUNSUPPORTED);
+    if (h->resident) {
+        if (cudaMalloc(&h->res_scratch, heat1d::resident_scratch_bytes(h->T, h->num_sms)) != cudaSuccess) {
+            cudaGetLastError();
+            set_error(nullptr, HEAT1D_ENOMEM, "resident scratch");
+            return bail(HEAT1D_ENOMEM);
         }
-    } else if (o.resident == 1) {
-        set_error(nullptr, HEAT1D_EUNSUPPORTED, "resident kernel needs one slab on one rank");
-        return bail(HEAT1D_EUNSUPPORTED);
     }
     *out = h;
     return HEAT1D_OK;

@@ -479,12 +479,12 @@ PassFn pass_fn(int kind) {
     return kind == 0 ? &k2_pass<V, NW, S, OPS> : kind == 1 ? &k2w_pass<V, NW, S, OPS> : &k2p_pass<V, NW, S, OPS>;
 }
 
-// (V, NW, S) instantiated for both kernel kinds and both arithmetic variants.
+// (V, NW, S) instantiated for all three kernel kinds and both arithmetic variants:
+// the defaults plus the tuning points the sweeps and tests use.
 #define HEAT1D_GEOMS(X)                                                                            \
-    X(9, 4, 3) X(9, 4, 4) X(9, 8, 3) X(9, 8, 4) X(17, 4, 2) X(17, 4, 3) X(17, 4, 4) X(17, 8, 2)  \
-    X(17, 8, 3) X(17, 8, 4) X(21, 4, 3) X(21, 8, 3) X(25, 4, 2) X(25, 4, 3) X(25, 4, 4) X(25, 8, 2) \
-    X(25, 8, 3) X(25, 8, 4) X(33, 4, 2) X(33, 4, 3) X(33, 8, 2) X(33, 8, 3) X(15, 8, 2) X(15, 8, 3)   \
-    X(17, 6, 2) X(17, 6, 3) X(17, 12, 2) X(17, 16, 2)
+    X(9, 4, 3) X(9, 8, 4) X(15, 8, 3) X(17, 4, 2) X(17, 4, 4) X(17, 8, 2) X(17, 8, 3) X(17, 8, 4)  \
+    X(17, 16, 2) X(21, 8, 3) X(25, 4, 3) X(25, 8, 2) X(33, 4, 2) X(33, 4, 3) X(33, 8, 2) X(33, 8, 3) \
+    X(49, 4, 3)
 
 PassFn lookup_pass(int V, int NW, int S, int ops, int kind) {
 #define X(v, nw, s)                                                                                \

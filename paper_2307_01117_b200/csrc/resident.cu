@@ -17,6 +17,7 @@
 // period parity: a span writes period p+2 edges only after its neighbours
 // published p+1, i.e. after they finished reading period p.
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -240,6 +241,7 @@ constexpr int RV = 17;        // cells per lane
 // warps per SM the register budget allows: ~100 regs (1 span/warp), ~156 (2 spans/warp)
 constexpr int MAX_WPS1 = 20, MAX_WPS2 = 12;
 constexpr int MAX_WPS = MAX_WPS1;
+constexpr int MAX_NW = 8;     // warps per CTA (__launch_bounds__(256))
 
 struct ResPlan {
     int64_t wt = 0, nw = 0, grid = 0;
@@ -293,7 +295,7 @@ bool res_plan(int ops, int64_t n, int T, int num_sms, ResPlan *p) {
     } else {
         const int64_t wps = (wt_min + num_sms - 1) / num_sms;
         if (wps > (p->spw == 1 ? MAX_WPS1 : MAX_WPS2)) return false;
-        const int64_t cps = wps > (p->spw == 1 ? 10 : 6) ? 2 : 1;
+        const int64_t cps = (wps + MAX_NW - 1) / MAX_NW;  // CTAs per SM (blocks <= 8 warps)
         p->nw = (wps + cps - 1) / cps;
         p->grid = (int64_t)num_sms * cps;
         p->wt = p->grid * p->nw;
@@ -344,6 +346,9 @@ cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int 
     void *args[] = {(void *)&A, (void *)&B, (void *)&n, (void *)&T, (void *)&nt, (void *)&r, (void *)&edges,
                     (void *)&flags, (void *)&Wt};
     if (warps_out) *warps_out = Wt;
+    if (getenv("HEAT1D_DEBUG"))
+        fprintf(stderr, "[heat1d] K6 n=%lld T=%d spw=%d Wt=%d nw=%lld grid=%lld smem=%zu\n", (long long)n, T,
+                p.spw, Wt, (long long)p.nw, (long long)p.grid, p.smem);
     return cudaLaunchCooperativeKernel(res_fn(ops, p.spw), dim3((unsigned)p.grid), dim3((unsigned)(p.nw * 32)),
                                        args, p.smem, st);
 }
