@@ -68,6 +68,15 @@ struct heat1d_s {
     ncclComm_t nccl = nullptr;
     void *alloc = nullptr;
 
+    // CUDA graphs of whole run(nt) pass sequences, keyed by (nt, starting buffer)
+    struct Graph {
+        int64_t nt;
+        int cur0, cur1;
+        int64_t launches;
+        cudaGraphExec_t exec;
+    };
+    std::vector<Graph> graphs;
+
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -317,6 +326,61 @@ int run_passes(heat1d_t h, int64_t nt) {
     }
     h->steps_done += nt;
     return HEAT1D_OK;
+}
+
+// Replay (or capture, then replay) the pass sequence of run(nt) as one CUDA
+// graph: one host submission per run instead of ~3 launches per pass.  Used
+// for K2 pass sequences (single slab, virtual slabs, NCCL); K6 is already one
+// launch and profiling needs per-launch events, so both bypass it.
+int run_maybe_graph(heat1d_t h, int64_t nt) {
+    const int64_t passes = (nt + h->T - 1) / h->T;
+    if (!h->use_graphs || h->prof || h->resident || passes < 2) return run_passes(h, nt);
+    for (auto &g : h->graphs) {
+        if (g.nt == nt && g.cur0 == h->cur) {
+            CK(cudaGraphLaunch(g.exec, h->stream));
+            h->cur = g.cur1;
+            h->steps_done += nt;
+            h->launches += g.launches;
+            return HEAT1D_OK;
+        }
+    }
+    const int cur0 = h->cur;
+    const int64_t l0 = h->launches, s0 = h->steps_done;
+    CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = run_passes(h, nt);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
+    cudaGraphExec_t exec = nullptr;
+    if (rc == HEAT1D_OK && e == cudaSuccess && graph &&
+        cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+        cudaGraphDestroy(graph);
+        heat1d_s::Graph g{nt, cur0, h->cur, h->launches - l0, exec};
+        if (h->graphs.size() >= 8) {
+            cudaGraphExecDestroy(h->graphs.front().exec);
+            h->graphs.erase(h->graphs.begin());
+        }
+        h->graphs.push_back(g);
+        h->cur = cur0;  // capture only recorded the work; replay it now
+        h->launches = l0;
+        h->steps_done = s0;
+        CK(cudaGraphLaunch(exec, h->stream));
+        h->cur = g.cur1;
+        h->launches += g.launches;
+        h->steps_done += nt;
+        return HEAT1D_OK;
+    }
+    // capture not possible here: run directly (clears the capture error state)
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    if (rc != HEAT1D_OK) {
+        if (!h->poisoned) return rc;
+        h->poisoned = 0;  // the failure was the capture, not the device
+    }
+    h->cur = cur0;
+    h->launches = l0;
+    h->steps_done = s0;
+    h->use_graphs = false;
+    return run_passes(h, nt);
 }
 
 int guard(heat1d_t h) {
@@ -654,7 +718,7 @@ int heat1d_run(heat1d_t h, int64_t nt) {
     if (!h->initialized) return set_error(h, HEAT1D_ESTATE, "run before set_initial");
     if (nt < 0) nt = h->nt_default;
     if (nt == 0) return HEAT1D_OK;
-    rc = run_passes(h, nt);
+    rc = run_maybe_graph(h, nt);
     if (rc) return rc;
     if (h->blocking) {
         CK(cudaStreamSynchronize(h->stream));
@@ -743,6 +807,7 @@ int heat1d_destroy(heat1d_t h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->comm) cudaStreamSynchronize(h->comm);
     if (h->nccl) ncclCommDestroy(h->nccl);
+    for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
     if (h->ev_ready) cudaEventDestroy(h->ev_ready);
     if (h->ev_halo) cudaEventDestroy(h->ev_halo);

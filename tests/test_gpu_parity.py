@@ -182,6 +182,28 @@ def test_split_run_invariance(h1):
     assert_bitwise(got, oracle.run(u0, 0.4, 42), "split")
 
 
+@pytest.mark.parametrize("vs", [1, 4])
+def test_graph_replay(h1, vs):
+    """run(nt) is captured once as a CUDA graph and replayed: repeated runs, both
+    starting buffers, and a fresh initial state must all stay exact."""
+    N, T = 300_007, 8
+    u0 = synth.uniform(55, 0, N, -1.0, 1.0)
+    with h1.Heat1D(N, 1, 0, 0.4, 1.0, 1.0, T=T, virtual_slabs=vs, resident=False) as h:
+        h.set_initial(u0)
+        for _ in range(3):
+            h.run(20)          # 3 passes: odd -> the next replay starts from the other buffer
+        h.run(7)
+        assert_bitwise(h.get(), oracle.run(u0, 0.4, 67), "graph replay vs=%d" % vs)
+        h.set_initial(u0)
+        h.run(20)
+        assert_bitwise(h.get(), oracle.run(u0, 0.4, 20), "graph replay after set_initial")
+        assert h.info()["launches"] > 0
+    with h1.Heat1D(N, 1, 0, 0.4, 1.0, 1.0, T=T, virtual_slabs=vs, resident=False, use_graphs=False) as h:
+        h.set_initial(u0)
+        h.run(20)
+        assert_bitwise(h.get(), oracle.run(u0, 0.4, 20), "no graphs")
+
+
 @pytest.mark.parametrize("G", [2, 3, 4, 8])
 @pytest.mark.parametrize("T", [1, 4, 8, 12])
 def test_virtual_slabs_multi_gpu_schedule(h1, G, T):
