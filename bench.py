@@ -41,7 +41,9 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     p.add_argument("--T", type=int, default=0)
-    p.add_argument("--mode", default="matched", choices=["matched", "fast"])
+    p.add_argument("--mode", default="fast", choices=["matched", "fast"],
+                   help="headline arithmetic: fast (north_star bound) or matched (bitwise = oracle)")
+    p.add_argument("--no-other-mode", action="store_true", help="skip timing the other mode")
     p.add_argument("--nt", type=int, default=0, help="override the config's nt (testing only)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -184,49 +186,73 @@ def emit(line, args):
 
 
 # ------------------------------------------------------------------ GPU arm
-def main():
-    args = parse()
-    from synth.configs import CONFIGS
-    cfg = CONFIGS[args.config]
-    if args.nt:
-        from dataclasses import replace
-        cfg = replace(cfg, nt=args.nt)
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+def kernel_roofline(info, cfg, count, world, steps, k2_launches, k2_ms, ms, value, mode):
+    """Roofline of the dominant kernel (K2 pass or K6 whole solve), this rank."""
+    if not k2_launches:
+        return None
+    hbm, peak_kind = peaks()
+    T = info["T"]
+    avg_ms = k2_ms / k2_launches
+    upd_launch = count * cfg.nt * steps / k2_launches       # cell updates per launch, this rank
+    steps_per_pass = cfg.nt if info["resident"] else T       # steps per HBM round trip of the state
+    alg_bytes = 16.0 * count * (upd_launch / count) / steps_per_pass  # 8 B read + 8 B written per cell per pass
+    hbm_term = hbm / (16.0 / steps_per_pass)                 # GLUPS bound by HBM (BASELINE.json)
+    fp64_term = FP64_TFLOPS * 1e3 / 4.0                      # GLUPS bound by FP64 peak / 4 flop
+    bj_roof = min(hbm_term, fp64_term) * world
+    kernel = ("k6_resident<V=17>" if info["resident"] else
+              ["k2_pass", "k2w_pass", "k2p_pass"][info["pass_kind"]] + "<V=%d,NW=%d,S=%d>" % (
+                  info["pass_V"], info["pass_NW"], info["pass_S"])) + "<OPS=%d>" % info["dp_ops"]
+    # the kernel's own bounds: HBM (16 B per cell per pass) and the fp64 pipe's issue rate
+    # 148 SM x 64 lanes x 1.965 GHz against its algorithmic fp64 instructions per update
+    # (dp_ops; the scaled fast variants add one rescale DMUL per cell per pass, DESIGN.md §6)
+    inst_per_upd = info["dp_ops"] + (1.0 / steps_per_pass if info["dp_ops"] <= 2 else 0.0)
+    pipe = SMS * FP64_LANES * SM_MHZ_MAX * 1e6 / 1e12        # T fp64 lane-instructions / s
+    alu_term = pipe * 1e3 / inst_per_upd                     # GLUPS
+    achieved_gbs = alg_bytes / (avg_ms / 1e3) / 1e9
+    dpi = inst_per_upd * upd_launch / (avg_ms / 1e3) / 1e12
+    if hbm_term <= alu_term:
+        roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
+                "frac": achieved_gbs / hbm, "peak_kind": peak_kind}
+    else:
+        roof = {"bound": "alu", "achieved": dpi, "peak": pipe, "unit": "Tinst/s (fp64 DFMA/DADD/DMUL)",
+                "frac": dpi / pipe, "peak_kind": "derived: 148 SM x 64 fp64 lanes x 1.965 GHz"}
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get("%s_T%d_%s" % (cfg.name, T, mode))
+    except Exception:
+        pass
+    roof.update({
+        "traffic": traffic, "kernel": kernel, "launches": k2_launches, "avg_launch_ms": avg_ms,
+        "steps_per_launch": upd_launch / count,
+        "alg_bytes_per_launch": alg_bytes, "alg_fp64_inst_per_launch": inst_per_upd * upd_launch,
+        "fp64_inst_per_update": inst_per_upd, "hbm_gbs_achieved": achieved_gbs,
+        "hbm_frac": achieved_gbs / hbm, "fp64_pipe_frac": dpi / pipe,
+        "kernel_roofline_glups": min(hbm_term, alu_term) * world,
+        "baseline_json_roofline_glups": bj_roof,
+        "baseline_json_frac": value / bj_roof,
+        "baseline_json_bound": "hbm" if hbm_term < fp64_term else "fp64 (37.2 TFLOP/s / 4 flop)",
+        "kernel_share_of_step": k2_ms / ms if world == 1 else None})
+    return roof
 
-    if args.impl == "reference":
-        reference_arm(args, cfg, rank)
-        return
 
+def fresh_nccl_id(h1, world, rank):
+    """One ncclUniqueId per communicator (each handle owns one), broadcast from rank 0."""
+    if world == 1:
+        return None
+    import torch.distributed as dist
+    obj = [h1.get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def measure(h1, cfg, mode, args, world, rank, local_rank, stream, u0_dev, with_e2e, sampler_on):
+    """Time K steps (after W warm-ups) of one full solve in `mode`; max over ranks."""
     import torch
     import torch.distributed as dist
-    from paper_2307_01117_b200 import _build
-    _build.build()
-    import paper_2307_01117_b200 as h1
-
-    torch.cuda.set_device(local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    stream = torch.cuda.current_stream()
-
-    nccl_id = None
-    if world > 1:
-        obj = [h1.get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
-
-    h = h1.Heat1D(cfg.nx, cfg.np, cfg.nt, cfg.k, cfg.dt, cfg.dx, T=args.T, mode=args.mode, rank=rank,
-                  nranks=world, nccl_id=nccl_id, device=local_rank, stream=stream)
+    h = h1.Heat1D(cfg.nx, cfg.np, cfg.nt, cfg.k, cfg.dt, cfg.dx, T=args.T, mode=mode, rank=rank,
+                  nranks=world, nccl_id=fresh_nccl_id(h1, world, rank), device=local_rank, stream=stream)
     first, count = h.local_range
-    # device-resident u0 for this slab (inputs in HBM before the timed region)
-    u0_dev = torch.empty(count, dtype=torch.float64, device="cuda")
-    if cfg.u0_kind == "uniform":
-        h.init_uniform(cfg.seed, cfg.lo, cfg.hi)
-        h.get(u0_dev)
-    else:
-        u0_dev.copy_(torch.from_numpy(cfg.u0(first, count)))
-    torch.cuda.synchronize()
 
     def step():
         h.set_initial(u0_dev)
@@ -240,7 +266,7 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    sampler = ClockSampler(range(world)) if rank == 0 else None
+    sampler = ClockSampler(range(world)) if (rank == 0 and sampler_on) else None
     launches0 = h.info()["launches"]
     h.set_profiling(True)
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -271,7 +297,7 @@ def main():
 
     # ---- end to end: pinned host u0 -> set_initial -> run -> get -> pinned host
     e2e = None
-    if not args.no_e2e:
+    if with_e2e:
         host_in = torch.empty(count, dtype=torch.float64, pin_memory=True)
         host_out = torch.empty(count, dtype=torch.float64, pin_memory=True)
         host_in.copy_(u0_dev)
@@ -297,48 +323,61 @@ def main():
                "d2h_bytes_per_step": 8 * count, "ms_per_step": ems / args.steps,
                "path": "heat1d_set_initial(pinned host) + heat1d_run + heat1d_get(pinned host)"}
         del host_in, host_out
+    roof = kernel_roofline(info, cfg, count, world, args.steps, k2_launches, k2_ms, ms, value, mode)
+    h.close()
+    return {"value": value, "ms": ms, "info": info, "roof": roof, "e2e": e2e, "clocks": clocks,
+            "launches": launches}
 
-    # ---- roofline of the dominant kernel (K2 pass), this rank
-    hbm, peak_kind = peaks()
-    T = info["T"]
-    roof = None
-    if k2_launches:
-        # dominant kernel: K2 (one T-step pass per launch) or K6 (the whole solve per launch)
-        avg_ms = k2_ms / k2_launches
-        upd_launch = count * cfg.nt * args.steps / k2_launches   # cell updates per launch, this rank
-        steps_per_pass = cfg.nt if info["resident"] else T        # steps per HBM round trip of the state
-        alg_bytes = 16.0 * count * (upd_launch / count) / steps_per_pass  # 8 B read + 8 B written per cell per pass
-        hbm_term = hbm / (16.0 / steps_per_pass)                 # GLUPS bound by HBM (BASELINE.json)
-        fp64_term = FP64_TFLOPS * 1e3 / 4.0                      # GLUPS bound by FP64 peak / 4 flop
-        bj_roof = min(hbm_term, fp64_term) * world
-        kernel = ("k6_resident<V=17>" if info["resident"] else
-                  ["k2_pass", "k2w_pass", "k2p_pass"][info["pass_kind"]] + "<V=%d,NW=%d,S=%d>" % (
-                      info["pass_V"], info["pass_NW"], info["pass_S"])) + "<OPS=%d>" % info["dp_ops"]
-        if hbm_term < fp64_term:
-            achieved = alg_bytes / (avg_ms / 1e3) / 1e9
-            roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                    "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes}
-        else:
-            # fp64-pipe bound: algorithmic fp64 instructions (dp_ops per update) per second against the
-            # pipe's issue rate 148 SM x 64 lanes x 1.965 GHz
-            dpi = info["dp_ops"] * upd_launch / (avg_ms / 1e3) / 1e12
-            peak = SMS * FP64_LANES * SM_MHZ_MAX * 1e6 / 1e12
-            roof = {"bound": "alu", "achieved": dpi, "peak": peak, "unit": "Tinst/s (fp64 DFMA/DADD/DMUL)",
-                    "frac": dpi / peak, "peak_kind": "derived: 148 SM x 64 fp64 lanes x 1.965 GHz",
-                    "alg_fp64_inst_per_launch": info["dp_ops"] * upd_launch, "alg_bytes_per_launch": alg_bytes}
-        traffic = None
-        try:
-            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-                traffic = json.load(f).get("%s_T%d_%s" % (cfg.name, T, args.mode))
-        except Exception:
-            pass
-        roof.update({
-            "traffic": traffic, "kernel": kernel, "launches": k2_launches, "avg_launch_ms": avg_ms,
-            "steps_per_launch": upd_launch / count,
-            "baseline_json_roofline_glups": bj_roof,
-            "baseline_json_frac": value / bj_roof,
-            "baseline_json_bound": "hbm" if hbm_term < fp64_term else "fp64 (37.2 TFLOP/s / 4 flop)",
-            "kernel_share_of_step": k2_ms / ms if world == 1 else None})
+
+def main():
+    args = parse()
+    from synth.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.nt:
+        from dataclasses import replace
+        cfg = replace(cfg, nt=args.nt)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        reference_arm(args, cfg, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2307_01117_b200 import _build
+    _build.build()
+    import paper_2307_01117_b200 as h1
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    stream = torch.cuda.current_stream()
+
+    # device-resident u0 for this rank's slab (inputs in HBM before the timed region)
+    first, count = h1.partition(cfg.nx, cfg.np, world, rank)
+    u0_dev = torch.empty(count, dtype=torch.float64, device="cuda")
+    if cfg.u0_kind == "uniform":
+        with h1.Heat1D(cfg.nx, cfg.np, 0, cfg.k, cfg.dt, cfg.dx, rank=rank, nranks=world,
+                       nccl_id=fresh_nccl_id(h1, world, rank), device=local_rank, stream=stream) as hg:
+            hg.init_uniform(cfg.seed, cfg.lo, cfg.hi)
+            hg.get(u0_dev)
+    else:
+        u0_dev.copy_(torch.from_numpy(cfg.u0(first, count)))
+    torch.cuda.synchronize()
+
+    main_m = measure(h1, cfg, args.mode, args, world, rank, local_rank, stream, u0_dev,
+                     not args.no_e2e, True)
+    other = None
+    if not args.no_other_mode:
+        om = "matched" if args.mode == "fast" else "fast"
+        o = measure(h1, cfg, om, args, world, rank, local_rank, stream, u0_dev, False, False)
+        other = {"mode": om, "value": o["value"], "ms_per_step": o["ms"] / args.steps,
+                 "dp_ops": o["info"]["dp_ops"], "T": o["info"]["T"], "gpu_launches": o["launches"],
+                 "roofline": o["roof"],
+                 "parity": "bitwise = oracle" if om == "matched" else "<= 1e-12*max|u0|*nt vs oracle"}
+    info = main_m["info"]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -349,21 +388,24 @@ def main():
             cpu = {"value": None, "unit": "GLUPS", "cores": 1, "kind": "oracle", "sample": "failed: %s" % e}
 
     if rank == 0:
+        ms = main_m["ms"]
         line = {
-            "metric": METRIC, "value": value, "unit": "GLUPS", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": main_m["value"], "unit": "GLUPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE.json %s recipe, seeded)" % cfg.name,
             "config": {"workload": cfg.name, "N": cfg.N, "nx": cfg.nx, "np": cfg.np, "nt": cfg.nt, "k": cfg.k,
-                       "dt": cfg.dt, "dx": cfg.dx, "r": info["r"], "T": T, "mode": args.mode,
+                       "dt": cfg.dt, "dx": cfg.dx, "r": info["r"], "T": info["T"], "mode": args.mode,
+                       "parity": ("bitwise = oracle" if args.mode == "matched"
+                                  else "<= 1e-12*max|u0|*nt vs oracle (north_star fast-mode bound)"),
                        "dp_ops": info["dp_ops"], "parallelism": "slabs%d" % world,
                        "l2": "inputs larger than L2" if 16 * cfg.N // world > 126 * 2 ** 20
                        else "L2-resident ring (no flush; each step re-reads u0 from HBM copy)",
                        "tile_cells": info["tile_cells"], "grid": info["grid"]},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
+            "roofline": main_m["roof"], "other_mode": other, "cpu_baseline": cpu, "e2e": main_m["e2e"],
+            "clocks": main_m["clocks"], "gpu_launches": main_m["launches"],
         }
         emit(line, args)
-    h.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -22,8 +22,11 @@
  *     every update is v = b + r*((a - 2b) + c), a=u[i-1], b=u[i], c=u[i+1],
  *     binary64 RNE.  HEAT1D_MODE_MATCHED evaluates exactly that sequence (the
  *     result is bitwise independent of T, np, the slab count and the GPU
- *     count, and bitwise equal to the CPU oracle); HEAT1D_MODE_FAST contracts
- *     the last multiply-add into one fma (error <= 1e-12*max|u0|*nt).
+ *     count, and bitwise equal to the CPU oracle); HEAT1D_MODE_FAST evaluates
+ *     the algebraically equal form u' = (1-2r)u_i + r(u_{i-1}+u_{i+1}) on the
+ *     scaled state v = u/r^t (one fp64 add per update at r = 1/2, add + fma
+ *     for 1/256 <= r < 1/2, rescaled once per T-step pass; else the contracted
+ *     3-op form), error <= 1e-12*max|u0|*nt (BASELINE.json north_star).
  *   - Threading: one host thread per handle.  A handle whose CUDA or NCCL
  *     call failed is "poisoned": every later call except heat1d_destroy
  *     returns the same error.
@@ -66,7 +69,7 @@ enum {
     HEAT1D_KERNEL_NAIVE = 1   /* one step per launch, modular indexing (K1; T forced to 1)    */
 };
 
-#define HEAT1D_T_MAX 32
+#define HEAT1D_T_MAX 64
 
 /* Options.  Always initialise with heat1d_opts_default(); `size` versions the struct. */
 typedef struct {
@@ -100,7 +103,7 @@ typedef struct {
     uint32_t size;          /* = sizeof(heat1d_info_t)                                     */
     int32_t T;              /* effective halo depth / steps per pass                        */
     int32_t mode, denominator, kernel;
-    int32_t dp_ops;         /* fp64 instructions per cell update in the pass kernel (3 or 4) */
+    int32_t dp_ops;         /* fp64 instructions per cell update in the pass kernel (1..4)  */
     int32_t nslabs;         /* slabs held by this handle (virtual_slabs, else 1)            */
     int32_t rank, nranks, device;
     double r;               /* k*dt/D as used by the kernels                                */

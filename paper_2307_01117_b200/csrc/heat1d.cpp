@@ -45,7 +45,10 @@ struct heat1d_s {
     int rank = 0, nranks = 1;
     int64_t nx = 0, np = 0, N = 0, nt_default = 0;
     double k = 0, dt = 0, dx = 0, r = 0;
+    double q = 0;  // per-step coefficient of the arithmetic variant (r, or c = (1-2r)/r scaled)
     int T = 8, mode = 0, den = 0, kernel = 0, ops = 4;
+    int ops_fast = 0;                    // scaled fast variant chosen at create (0: none)
+    unsigned long long *absmax = nullptr;  // device word for K5 (fast mode range check)
     bool blocking = true, use_graphs = true;
     int64_t pad = 16;
     int64_t first = 0, count = 0;  // this rank's range (union of its slabs)
@@ -167,12 +170,13 @@ int64_t min_slab(int64_t nx, int64_t np, int32_t G) {
 }
 
 int auto_T(int ops) {
-    // DESIGN.md §6 (T sweeps in profiles/): throughput rises with T up to the
-    // largest halo the kernels support, because each pass moves 16/T bytes per
-    // update and the freed HBM power lets the SM clock rise under the 1 kW cap;
-    // past T ~ 12 (4-op) / 16 (3-op) the pass is fp64-issue bound.
-    (void)ops;
-    return HEAT1D_T_MAX;
+    // DESIGN.md §6 (T sweeps in profiles/r01_tsweep_*.jsonl): each pass moves
+    // 16/T bytes per update, so T is raised until the pass is fp64-issue bound
+    // and the extra trapezoid work (2T/(32V) per warp) starts to cost more than
+    // the HBM power it frees under the 1 kW cap: 32 for the 3/4-op matched
+    // forms, 48 for the 2-op scaled form, 64 for the 1-op form at r = 1/2 (the
+    // only variant still HBM-bound at T = 32).
+    return ops == 1 ? 64 : ops == 2 ? 48 : 32;
 }
 
 bool parse_geom_env(PassGeom *g) {
@@ -219,7 +223,7 @@ int launch_pass_slab(heat1d_t h, const Slab &s, int Tp, int64_t lo, int64_t hi, 
     }
     int grid = 0;
     CK(heat1d::launch_pass(h->geom, h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp, lo, hi,
-                           wrapT, h->r, h->num_sms, h->stream, &grid));
+                           wrapT, h->q, heat1d::scale_of(h->r, Tp), h->num_sms, h->stream, &grid));
     if (grid > 0) h->launches++;
     h->last_grid = grid > 0 ? grid : h->last_grid;
     if (h->prof) CK(cudaEventRecord(e1, h->stream));
@@ -266,8 +270,8 @@ int run_resident(heat1d_t h, int64_t nt) {
         if (!e0 || !e1) return set_error(h, HEAT1D_ECUDA, "event pool");
         CK(cudaEventRecord(e0, h->stream));
     }
-    CK(heat1d::launch_resident(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, h->T, nt, h->r,
-                               h->res_scratch, h->num_sms, h->stream, &h->res_warps));
+    CK(heat1d::launch_resident(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, h->T, nt, h->q,
+                               h->r, h->res_scratch, h->num_sms, h->stream, &h->res_warps));
     h->launches++;
     if (h->prof) CK(cudaEventRecord(e1, h->stream));
     h->cur ^= 1;
@@ -290,8 +294,9 @@ int run_passes(heat1d_t h, int64_t nt) {
                 e1 = prof_event(h);
                 CK(cudaEventRecord(e0, h->stream));
             }
-            CK(heat1d::launch_naive(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, h->r,
-                                    h->stream));
+            // one step per launch: the scaled variants degenerate to their unscaled fast form
+            CK(heat1d::launch_naive(heat1d::ops_scaled(h->ops) ? 3 : h->ops, cell0(h, s, h->cur),
+                                    cell0(h, s, h->cur ^ 1), s.count, h->r, h->stream));
             if (h->prof) CK(cudaEventRecord(e1, h->stream));
             h->launches++;
             h->cur ^= 1;
@@ -316,8 +321,8 @@ int run_passes(heat1d_t h, int64_t nt) {
             }
             CK(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
             for (const Slab &s : h->slabs) {
-                CK(heat1d::launch_edges(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp, h->r,
-                                        h->stream));
+                CK(heat1d::launch_edges(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp, h->q,
+                                        heat1d::scale_of(h->r, Tp), h->stream));
                 h->launches++;
             }
         }
@@ -459,7 +464,7 @@ int64_t heat1d_buffer_len(int64_t nx, int64_t np, const heat1d_opts *o) {
     }
     const int G = o->virtual_slabs > 1 ? o->virtual_slabs : o->nranks;
     const int rank = o->virtual_slabs > 1 ? -1 : o->rank;
-    const int T = o->T > 0 ? o->T : 12;
+    const int T = o->T > 0 ? o->T : HEAT1D_T_MAX;  // auto T never exceeds the maximum
     const int64_t pad = pad_for(T);
     int64_t total = 0, f, c;
     for (int g = 0; g < G; ++g) {
@@ -542,6 +547,21 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     h->use_graphs = o.use_graphs != 0;
     h->ops = (o.mode == HEAT1D_MODE_FAST || is_pow2(r) || r == 0.0) ? 3 : 4;
     // r == 0: fma(0, t, b) == b + 0*t == b for finite t (identity either way)
+    // Fast mode works on the scaled state v = u / r^t (stencil.cuh, DESIGN.md §3 c21): 1 DP op per
+    // update at r = 1/2, 2 for 1/256 <= r < 1/2 (the state grows by at most r^-T <= 2^512 within a
+    // pass, T <= 64; select_fast_ops checks max|u0| against it).  Outside that range (tiny r,
+    // unstable r > 1/2) the 3-op contracted form.
+    if (o.mode == HEAT1D_MODE_FAST && o.kernel != HEAT1D_KERNEL_NAIVE) {
+        if (r == 0.5)
+            h->ops = 1;
+        else if (r >= 1.0 / 256.0 && r < 0.5)
+            h->ops = 2;
+    }
+    if (heat1d::ops_scaled(h->ops)) {
+        h->ops_fast = h->ops;
+        h->ops = 3;  // until set_initial has checked the range of u0 (after_initial)
+    }
+    h->q = r;
     auto bail = [&](int rc) {
         heat1d_destroy(h);
         return rc;
@@ -563,18 +583,19 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
 
     // T and the kernel family.  K6 (whole solve on chip) for one slab on one rank
     // when the ring fits; otherwise K2 passes.
-    int T = o.T > 0 ? o.T : auto_T(h->ops);
+    int T = o.T > 0 ? o.T : auto_T(h->ops_fast ? h->ops_fast : h->ops);
     if (o.kernel == HEAT1D_KERNEL_NAIVE) T = 1;
     if (T > mslab) T = (int)mslab;  // a slab must hold its own halo
     const bool res_ok = (G == 1 && o.kernel == HEAT1D_KERNEL_AUTO && o.resident != 0);
     if (res_ok) {
         const int64_t n0 = h->N;
-        int Tr = o.T > 0 ? o.T : 32;  // K6 period: halo refresh every 32 steps
+        int Tr = (o.T > 0 && o.T < 32) ? o.T : 32;  // K6 period: halo refresh every <= 32 steps (one lane per halo cell)
         if (Tr > n0) Tr = (int)n0;
         int coop = 0;
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
         const bool fits = coop && n0 <= heat1d::resident_capacity(Tr, h->num_sms) && n0 >= Tr &&
-                          heat1d::resident_fits(h->ops, n0, Tr, h->num_sms);
+                          heat1d::resident_fits(h->ops, n0, Tr, h->num_sms) &&
+                          (!h->ops_fast || heat1d::resident_fits(h->ops_fast, n0, Tr, h->num_sms));
         cudaGetLastError();
         if (fits) {
             h->resident = true;
@@ -657,6 +678,11 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
         }
     }
     if (!parse_geom_env(&h->geom)) h->geom = heat1d::choose_geom(h->slabs[0].count, h->T, h->num_sms);
+    if (h->ops_fast && cudaMalloc(&h->absmax, sizeof(unsigned long long)) != cudaSuccess) {
+        cudaGetLastError();
+        set_error(nullptr, HEAT1D_ENOMEM, "absmax word");
+        return bail(HEAT1D_ENOMEM);
+    }
     if (h->resident) {
         if (cudaMalloc(&h->res_scratch, heat1d::resident_scratch_bytes(h->T, h->num_sms)) != cudaSuccess) {
             cudaGetLastError();
@@ -675,12 +701,42 @@ int heat1d_local_range(heat1d_t h, int64_t *first, int64_t *count) {
     return HEAT1D_OK;
 }
 
+// Fast mode: the scaled state of a pass reaches at most max|u0| * r^-T (max
+// principle, r <= 1/2).  Use the scaled variant only while that stays below
+// 2^1000 (checked by K5 on every new initial state), else the 3-op form.
+static int select_fast_ops(heat1d_t h) {
+    if (!h->ops_fast) return HEAT1D_OK;
+    CK(cudaMemsetAsync(h->absmax, 0, sizeof(unsigned long long), h->stream));
+    for (const Slab &s : h->slabs) {
+        CK(heat1d::launch_absmax(cell0(h, s, h->cur), s.count, h->absmax, h->stream));
+        h->launches++;
+    }
+    unsigned long long bits = 0;
+    CK(cudaMemcpyAsync(&bits, h->absmax, sizeof bits, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    double m;
+    memcpy(&m, &bits, sizeof m);
+    int e = 0;
+    if (std::isfinite(m)) std::frexp(m, &e);
+    const bool ok = std::isfinite(m) && (double)e + (double)h->T * std::log2(1.0 / h->r) < 1000.0;
+    const int want = ok ? h->ops_fast : 3;
+    if (want != h->ops) {
+        h->ops = want;
+        h->q = heat1d::ops_scaled(want) ? (1.0 - 2.0 * h->r) / h->r : h->r;
+        for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);  // they bake in the variant
+        h->graphs.clear();
+    }
+    return HEAT1D_OK;
+}
+
 static int after_initial(heat1d_t h) {
     if (!h->multi()) {
         const Slab &s = h->slabs[0];
         CK(heat1d::launch_wrap_fill(cell0(h, s, h->cur), s.count, h->pad, h->stream));
         h->launches++;
     }
+    int rc = select_fast_ops(h);
+    if (rc) return rc;
     CK(cudaStreamSynchronize(h->stream));
     h->initialized = true;
     h->steps_done = 0;
@@ -815,6 +871,7 @@ int heat1d_destroy(heat1d_t h) {
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     if (h->alloc) cudaFree(h->alloc);
     if (h->res_scratch) cudaFree(h->res_scratch);
+    if (h->absmax) cudaFree(h->absmax);
     delete h;
     return HEAT1D_OK;
 }

@@ -117,8 +117,9 @@ __device__ __forceinline__ void warp_step(const double (&u)[V], double (&v)[V], 
 
 // T steps in registers, ping-pong between u and a scratch array (no moves
 // inside the loop); the result is left in u.
+// Scaled variants (OPS <= 2) end the pass with u = v * r^T (`scale`, stencil.cuh).
 template <int V, int OPS>
-__device__ __forceinline__ void warp_steps(double (&u)[V], int T, double r) {
+__device__ __forceinline__ void warp_steps(double (&u)[V], int T, double r, double scale) {
     double v[V];
     int s = 0;
     for (; s + 2 <= T; s += 2) {
@@ -129,6 +130,10 @@ __device__ __forceinline__ void warp_steps(double (&u)[V], int T, double r) {
         warp_step<V, OPS>(u, v, r);
 #pragma unroll
         for (int j = 0; j < V; ++j) u[j] = v[j];
+    }
+    if constexpr (ops_scaled(OPS)) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) u[j] = __dmul_rn(u[j], scale);
     }
 }
 
@@ -147,7 +152,7 @@ __device__ __forceinline__ void warp_steps(double (&u)[V], int T, double r) {
 template <int V, int NW, int S, int OPS>
 __global__ void __launch_bounds__(NW * 32)
 k2_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t out_lo,
-        int64_t out_hi, int wrapT, double r, int64_t ntiles, uint32_t stage_doubles) {
+        int64_t out_hi, int wrapT, double r, double scale, int64_t ntiles, uint32_t stage_doubles) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);
     double *stages = reinterpret_cast<double *>(smem_raw + 128);
@@ -209,7 +214,7 @@ k2_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, 
 
         __syncthreads();  // B1: every warp has its span in registers -> in-place writes are safe
 
-        warp_steps<V, OPS>(u, T, r);
+        warp_steps<V, OPS>(u, T, r, scale);
 
 #pragma unroll
         for (int j = 0; j < V; ++j) {
@@ -253,7 +258,7 @@ k2_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, 
 template <int V, int NW, int S, int OPS>
 __global__ void __launch_bounds__(NW * 32)
 k2w_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t out_lo,
-         int64_t out_hi, int wrapT, double r, int64_t nspans, uint32_t slot_doubles) {
+         int64_t out_hi, int wrapT, double r, double scale, int64_t nspans, uint32_t slot_doubles) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int BAR_BYTES = ((NW * S * 8 + 127) / 128) * 128;
     const int lane = threadIdx.x & 31;
@@ -309,7 +314,7 @@ k2w_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
 #pragma unroll
         for (int j = 0; j < V; ++j) u[j] = st[base + j];
 
-        warp_steps<V, OPS>(u, T, r);
+        warp_steps<V, OPS>(u, T, r, scale);
 
         // each lane rewrites only its own cells: no intra-warp WAR hazard
 #pragma unroll
@@ -354,7 +359,7 @@ k2w_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
 template <int V, int NW, int S, int OPS>
 __global__ void __launch_bounds__((NW + 1) * 32)
 k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t out_lo,
-         int64_t out_hi, int wrapT, double r, int64_t ntiles, uint32_t stage_doubles) {
+         int64_t out_hi, int wrapT, double r, double scale, int64_t ntiles, uint32_t stage_doubles) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);
     uint64_t *done = full + S;
@@ -446,7 +451,7 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
 #pragma unroll
         for (int j = 0; j < V; ++j) u[j] = st[base + j];
         asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");  // B1 among compute warps
-        warp_steps<V, OPS>(u, T, r);
+        warp_steps<V, OPS>(u, T, r, scale);
 #pragma unroll
         for (int j = 0; j < V; ++j) {
             const int p = lane * V + j;
@@ -471,8 +476,8 @@ size_t PassGeom::smem_bytes(int T) const {
 
 namespace {
 
-using PassFn = void (*)(const double *, double *, int64_t, int, int64_t, int64_t, int, double, int64_t,
-                        uint32_t);
+using PassFn = void (*)(const double *, double *, int64_t, int, int64_t, int64_t, int, double, double,
+                        int64_t, uint32_t);
 
 template <int V, int NW, int S, int OPS>
 PassFn pass_fn(int kind) {
@@ -486,11 +491,23 @@ PassFn pass_fn(int kind) {
     X(17, 16, 2) X(21, 8, 3) X(25, 4, 3) X(25, 8, 2) X(33, 4, 2) X(33, 4, 3) X(33, 8, 2) X(33, 8, 3) \
     X(49, 4, 3)
 
+// The scaled fast-mode variants (OPS 2, 1) exist for the producer-warp kind only,
+// at the default geometries and the tuning points of the fast-mode sweeps.
+#define HEAT1D_GEOMS_SCALED(X) X(9, 4, 3) X(17, 8, 3) X(25, 4, 3) X(33, 4, 3) X(33, 8, 3) X(49, 4, 3)
+
 PassFn lookup_pass(int V, int NW, int S, int ops, int kind) {
+    if (ops == 4 || ops == 3) {
 #define X(v, nw, s)                                                                                \
     if (V == v && NW == nw && S == s)                                                              \
         return ops == 4 ? pass_fn<v, nw, s, 4>(kind) : pass_fn<v, nw, s, 3>(kind);
-    HEAT1D_GEOMS(X)
+        HEAT1D_GEOMS(X)
+#undef X
+        return nullptr;
+    }
+    if (kind != 2) return nullptr;
+#define X(v, nw, s)                                                                                \
+    if (V == v && NW == nw && S == s) return ops == 2 ? &k2p_pass<v, nw, s, 2> : &k2p_pass<v, nw, s, 1>;
+    HEAT1D_GEOMS_SCALED(X)
 #undef X
     return nullptr;
 }
@@ -508,7 +525,7 @@ PassGeom choose_geom(int64_t n_out, int T, int num_sms) {
 }
 
 cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, int64_t n, int T,
-                        int64_t out_lo, int64_t out_hi, int wrapT, double r, int num_sms,
+                        int64_t out_lo, int64_t out_hi, int wrapT, double q, double scale, int num_sms,
                         cudaStream_t st, int *grid_out) {
     PassFn fn = lookup_pass(g.V, g.NW, g.S, ops, g.kind);
     if (!fn) return cudaErrorInvalidConfiguration;
@@ -553,7 +570,7 @@ cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, 
     const int64_t need = g.kind != 1 ? units : (units + g.NW - 1) / g.NW;
     if (grid > need) grid = need;
     if (grid_out) *grid_out = (int)grid;
-    fn<<<(unsigned)grid, threads, smem, st>>>(A, B, n, T, out_lo, out_hi, wrapT, r, units, stage_doubles);
+    fn<<<(unsigned)grid, threads, smem, st>>>(A, B, n, T, out_lo, out_hi, wrapT, q, scale, units, stage_doubles);
     return cudaGetLastError();
 }
 
@@ -584,8 +601,8 @@ cudaError_t launch_naive(int ops, const double *A, double *B, int64_t n, double 
 // The 3T-cell window shrinks by one cell per side per step (light cone).
 template <int OPS>
 __global__ void __launch_bounds__(96) k3_edges(const double *__restrict__ A, double *__restrict__ B, int64_t n,
-                                               int T, double r) {
-    __shared__ double w[2][3 * 32];
+                                               int T, double r, double scale) {
+    __shared__ double w[2][3 * 64];
     const int64_t base = (blockIdx.x == 0) ? -(int64_t)T : n - 2 * (int64_t)T;
     const int len = 3 * T;
     for (int i = threadIdx.x; i < len; i += blockDim.x) w[0][i] = A[base + i];
@@ -598,15 +615,23 @@ __global__ void __launch_bounds__(96) k3_edges(const double *__restrict__ A, dou
         cur ^= 1;
         __syncthreads();
     }
-    for (int i = threadIdx.x; i < T; i += blockDim.x) B[base + T + i] = w[cur][T + i];
+    for (int i = threadIdx.x; i < T; i += blockDim.x) {
+        double x = w[cur][T + i];
+        if constexpr (ops_scaled(OPS)) x = __dmul_rn(x, scale);
+        B[base + T + i] = x;
+    }
 }
 
-cudaError_t launch_edges(int ops, const double *A, double *B, int64_t n, int T, double r, cudaStream_t st) {
-    if (T < 1 || T > 32) return cudaErrorInvalidValue;
-    if (ops == 4)
-        k3_edges<4><<<2, 96, 0, st>>>(A, B, n, T, r);
-    else
-        k3_edges<3><<<2, 96, 0, st>>>(A, B, n, T, r);
+cudaError_t launch_edges(int ops, const double *A, double *B, int64_t n, int T, double q, double scale,
+                         cudaStream_t st) {
+    if (T < 1 || T > 64) return cudaErrorInvalidValue;
+    switch (ops) {
+        case 4: k3_edges<4><<<2, 96, 0, st>>>(A, B, n, T, q, scale); break;
+        case 3: k3_edges<3><<<2, 96, 0, st>>>(A, B, n, T, q, scale); break;
+        case 2: k3_edges<2><<<2, 96, 0, st>>>(A, B, n, T, q, scale); break;
+        case 1: k3_edges<1><<<2, 96, 0, st>>>(A, B, n, T, q, scale); break;
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 
@@ -621,6 +646,34 @@ __global__ void k4_wrap_fill(double *A, int64_t n, int64_t pad) {
 
 cudaError_t launch_wrap_fill(double *A, int64_t n, int64_t pad, cudaStream_t st) {
     k4_wrap_fill<<<1, 128, 0, st>>>(A, n, pad);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K5
+// max |u| over a slab, as the bit pattern of a non-negative double (those order
+// like unsigned integers; inf and NaN sort above every finite value).  Used once
+// per initial state to check the fast mode's scaled-state range.
+__global__ void __launch_bounds__(256) k5_absmax(const double *__restrict__ u, int64_t count,
+                                                 unsigned long long *out) {
+    unsigned long long m = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(u[i]) & 0x7fffffffffffffffull;
+        m = b > m ? b : m;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(0xffffffffu, m, o);
+        m = x > m ? x : m;
+    }
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+cudaError_t launch_absmax(const double *u, int64_t count, unsigned long long *out, cudaStream_t st) {
+    if (count <= 0) return cudaSuccess;
+    int64_t blocks = (count + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    k5_absmax<<<(unsigned)blocks, 256, 0, st>>>(u, count, out);
     return cudaGetLastError();
 }
 

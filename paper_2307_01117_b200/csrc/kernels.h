@@ -7,7 +7,19 @@
 namespace heat1d {
 
 // Arithmetic variants of Eq. 2 (see stencil.cuh).
-enum Ops { OPS_MATCHED4 = 4, OPS_FMA3 = 3 };
+enum Ops { OPS_MATCHED4 = 4, OPS_FMA3 = 3, OPS_SCALED2 = 2, OPS_SCALED1 = 1 };
+
+// Scaled variants work on v = u / r^t: true iff a pass must end with u = v * r^T'.
+__host__ __device__ constexpr bool ops_scaled(int ops) { return ops <= 2; }
+
+// r^T' as the left-to-right product ((1*r)*r)*...  -- host and device evaluate
+// the same sequence of IEEE products, so every kernel rescales by the same bits.
+__host__ __device__ inline double scale_of(double r, int Tp) {
+    double s = 1.0;
+    for (int i = 0; i < Tp; ++i) s = s * r;
+    return s;
+}
+
 
 // Geometry of the temporal-blocked pass kernel (K2) for one launch config.
 struct PassGeom {
@@ -31,19 +43,23 @@ PassGeom choose_geom(int64_t n_out, int T, int num_sms);
 // offsets and at [n, n+pad)).  Reads A[out_lo-T, out_hi+T), writes B[out_lo, out_hi).
 // wrapT > 0 (single-slab ring): cells [0,wrapT) are also written to
 // B[n, n+wrapT) and cells [n-wrapT, n) to B[-wrapT, 0)  (periodic self-halo).
+// q = the variant's per-step coefficient, scale = r^T (scaled variants only; stencil.cuh).
 cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, int64_t n,
-                        int T, int64_t out_lo, int64_t out_hi, int wrapT, double r,
+                        int T, int64_t out_lo, int64_t out_hi, int wrapT, double q, double scale,
                         int num_sms, cudaStream_t st, int *grid_out);
 
 // K1: one step over the whole ring with modular indexing (no pads used).
 cudaError_t launch_naive(int ops, const double *A, double *B, int64_t n, double r, cudaStream_t st);
 
 // K3: the two edge strips [0,T) and [n-T,n) of a slab after its ghosts arrived.
-cudaError_t launch_edges(int ops, const double *A, double *B, int64_t n, int T, double r,
+cudaError_t launch_edges(int ops, const double *A, double *B, int64_t n, int T, double q, double scale,
                          cudaStream_t st);
 
 // K4: fill `pad` ghost cells on each side of a single-slab ring, modularly.
 cudaError_t launch_wrap_fill(double *A, int64_t n, int64_t pad, cudaStream_t st);
+
+// K5: *out = max(*out, bits of max |u[i]|)  (caller zeroes *out first).
+cudaError_t launch_absmax(const double *u, int64_t count, unsigned long long *out, cudaStream_t st);
 
 // K0: u[i] = lo + (hi-lo) * U(seed, first+i), splitmix64 counter form.
 cudaError_t launch_init_uniform(double *u, int64_t count, int64_t first, uint64_t seed,
@@ -53,7 +69,7 @@ cudaError_t launch_init_uniform(double *u, int64_t count, int64_t first, uint64_
 int64_t resident_capacity(int T, int num_sms);
 bool resident_fits(int ops, int64_t n, int T, int num_sms);  // plan + co-residency check
 size_t resident_scratch_bytes(int T, int num_sms);
-cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double r,
-                            void *scratch, int num_sms, cudaStream_t st, int *warps_out);
+cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
+                            double r, void *scratch, int num_sms, cudaStream_t st, int *warps_out);
 
 }  // namespace heat1d

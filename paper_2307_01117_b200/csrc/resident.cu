@@ -63,9 +63,9 @@ __device__ __forceinline__ void step_regs(const double (&u)[V], double (&v)[V], 
     }
 }
 
-// Tp steps on u (v is scratch), result in u.
+// Tp steps on u (v is scratch), result in u; scaled variants end with u *= r^Tp.
 template <int V, int OPS, bool EARLY>
-__device__ __forceinline__ void steps_regs(double (&u)[V], double (&v)[V], int Tp, double r) {
+__device__ __forceinline__ void steps_regs(double (&u)[V], double (&v)[V], int Tp, double r, double scale) {
     double L = 0.0, R = 0.0;
     if constexpr (EARLY) {
         L = __shfl_up_sync(0xffffffffu, u[V - 1], 1);
@@ -80,6 +80,10 @@ __device__ __forceinline__ void steps_regs(double (&u)[V], double (&v)[V], int T
         step_regs<V, OPS, EARLY>(u, v, L, R, r);
 #pragma unroll
         for (int j = 0; j < V; ++j) u[j] = v[j];
+    }
+    if constexpr (ops_scaled(OPS)) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) u[j] = __dmul_rn(u[j], scale);
     }
 }
 
@@ -173,7 +177,7 @@ __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, const 
 template <int V, int OPS, int SPW, bool EARLY>
 __global__ void __launch_bounds__(256)
 k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t nt, double r,
-            double *__restrict__ edges, unsigned *__restrict__ flags, int Wt) {
+            double rr, double *__restrict__ edges, unsigned *__restrict__ flags, int Wt) {
     extern __shared__ __align__(16) double srow[];
     const int lane = threadIdx.x & 31;
     const int wib = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);  // warp-uniform for the compiler
@@ -183,6 +187,8 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
     double *rows = srow + (size_t)wib * SPW * (32 * V + 1);
     const Span a = make_span(gw, Ns, n, rows);
     double ua[V], v[V];
+    // scaled variants: r is their coefficient c, rr the true r; r^T per full period
+    const double scaleT = ops_scaled(OPS) ? scale_of(rr, T) : 1.0;
     load_span<V>(a, A, n, T, lane);
     row_to_regs<V>(a.row, ua, lane);
 
@@ -190,7 +196,8 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
         int64_t done = 0;
         for (unsigned p = 0;; ++p) {
             const int Tp = (int)((nt - done) < T ? (nt - done) : T);
-            steps_regs<V, OPS, EARLY>(ua, v, Tp, r);
+            const double sc = (ops_scaled(OPS) && Tp != T) ? scale_of(rr, Tp) : scaleT;
+            steps_regs<V, OPS, EARLY>(ua, v, Tp, r, sc);
             regs_to_row<V>(ua, a.row, lane);
             done += Tp;
             if (done >= nt) break;
@@ -212,14 +219,15 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
         for (unsigned p = 0;; ++p) {
             const int Tp = (int)((nt - done) < T ? (nt - done) : T);
             const bool last = done + Tp >= nt;
-            steps_regs<V, OPS, EARLY>(ua, v, Tp, r);  // A: halos valid for period p
+            const double sc = (ops_scaled(OPS) && Tp != T) ? scale_of(rr, Tp) : scaleT;
+            steps_regs<V, OPS, EARLY>(ua, v, Tp, r, sc);  // A: halos valid for period p
             regs_to_row<V>(ua, a.row, lane);
             if (!last) publish(a, T, p, edges, flags, lane);
             if (p > 0) {  // B's halos for period p: neighbours' period p-1 edges
                 refresh(b, T, p - 1, edges, flags, lane);
                 row_to_regs<V>(b.row, ub, lane);
             }
-            steps_regs<V, OPS, EARLY>(ub, v, Tp, r);
+            steps_regs<V, OPS, EARLY>(ub, v, Tp, r, sc);
             regs_to_row<V>(ub, b.row, lane);
             if (!last) publish(b, T, p, edges, flags, lane);
             done += Tp;
@@ -257,13 +265,15 @@ int res_early() {
 const void *res_fn(int ops, int spw) {
     const bool early = res_early() != 0;
 #define RF(o, s, e) (const void *)&k6_resident<RV, o, s, e>
-    if (spw == 1) return early ? (ops == 4 ? RF(4, 1, true) : RF(3, 1, true)) : (ops == 4 ? RF(4, 1, false) : RF(3, 1, false));
-    return early ? (ops == 4 ? RF(4, 2, true) : RF(3, 2, true)) : (ops == 4 ? RF(4, 2, false) : RF(3, 2, false));
+#define RF_OPS(s, e) (ops == 4 ? RF(4, s, e) : ops == 3 ? RF(3, s, e) : ops == 2 ? RF(2, s, e) : RF(1, s, e))
+    if (spw == 1) return early ? RF_OPS(1, true) : RF_OPS(1, false);
+    return early ? RF_OPS(2, true) : RF_OPS(2, false);
+#undef RF_OPS
 #undef RF
 }
 
 cudaError_t res_attr(const void *fn) {
-    static const void *done[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    static const void *done[16] = {nullptr};
     for (const void *d : done)
         if (d == fn) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -333,8 +343,8 @@ size_t resident_scratch_bytes(int T, int num_sms) {
     return (size_t)ns * 4 * T * sizeof(double) + (size_t)ns * sizeof(unsigned) + 256;
 }
 
-cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double r,
-                            void *scratch, int num_sms, cudaStream_t st, int *warps_out) {
+cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
+                            double r, void *scratch, int num_sms, cudaStream_t st, int *warps_out) {
     ResPlan p;
     if (!res_plan(ops, n, T, num_sms, &p)) return cudaErrorInvalidValue;
     const int64_t ns = p.wt * p.spw;
@@ -343,8 +353,8 @@ cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int 
     cudaError_t e = cudaMemsetAsync(flags, 0, (size_t)ns * sizeof(unsigned), st);
     if (e != cudaSuccess) return e;
     int Wt = (int)p.wt;
-    void *args[] = {(void *)&A, (void *)&B, (void *)&n, (void *)&T, (void *)&nt, (void *)&r, (void *)&edges,
-                    (void *)&flags, (void *)&Wt};
+    void *args[] = {(void *)&A, (void *)&B, (void *)&n, (void *)&T, (void *)&nt, (void *)&q, (void *)&r,
+                    (void *)&edges, (void *)&flags, (void *)&Wt};
     if (warps_out) *warps_out = Wt;
     if (getenv("HEAT1D_DEBUG"))
         fprintf(stderr, "[heat1d] K6 n=%lld T=%d spw=%d Wt=%d nw=%lld grid=%lld smem=%zu\n", (long long)n, T,

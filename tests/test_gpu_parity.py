@@ -44,7 +44,7 @@ def assert_bitwise(got, want, what=""):
 
 
 # ------------------------------------------------------------------ C1
-@pytest.mark.parametrize("T", [0, 1, 2, 3, 4, 5, 8, 12, 16, 31, 32])
+@pytest.mark.parametrize("T", [0, 1, 2, 3, 4, 5, 8, 12, 16, 31, 32, 33, 48, 64])
 def test_c1_bitwise_all_T(h1, T):
     r = oracle.r_of(C1.k, C1.dt, C1.dx)
     want = oracle.run(C1.u0(), r, C1.nt)
@@ -167,6 +167,8 @@ def test_cross_T_bitwise(h1):
     for T in [1, 2, 3, 4, 6, 8, 11, 12, 16, 24, 32]:
         for res in (False, True):
             assert_bitwise(gpu_run(h1, u0, N, 1, nt, 0.4, T=T, resident=res), ref, "T=%d res=%s" % (T, res))
+    for T in [33, 40, 48, 63, 64]:
+        assert_bitwise(gpu_run(h1, u0, N, 1, nt, 0.4, T=T, resident=False), ref, "T=%d" % T)
 
 
 def test_split_run_invariance(h1):
@@ -205,7 +207,7 @@ def test_graph_replay(h1, vs):
 
 
 @pytest.mark.parametrize("G", [2, 3, 4, 8])
-@pytest.mark.parametrize("T", [1, 4, 8, 12])
+@pytest.mark.parametrize("T", [1, 4, 8, 12, 32, 64])
 def test_virtual_slabs_multi_gpu_schedule(h1, G, T):
     """The multi-GPU schedule (exchange || interior, then edges) with the
     transport replaced by device copies between G slabs on one GPU."""
@@ -231,6 +233,116 @@ def test_fast_mode_within_bound(h1):
     got = gpu_run(h1, u0, N, 1, nt, 0.4, mode="fast")
     err = np.max(np.abs(got - want))
     assert err <= 1e-12 * np.max(np.abs(u0)) * nt, err
+
+
+def fast_bound(u0, nt):
+    """north_star: max|u_gpu - u_oracle| <= 1e-12 * max|u| * nt (max|u| = max|u0|, reading c16)."""
+    return 1e-12 * float(np.max(np.abs(u0))) * nt
+
+
+# (k, expected dp_ops): r = 1/2 -> one add per update; 1/256 <= r < 1/2 -> add + fma on the
+# scaled state; tiny r and unstable r > 1/2 -> the contracted 3-op form
+FAST_CASES = [(0.5, 1), (0.25, 2), (0.4, 2), (0.01, 2), (1.0 / 256, 2), (0.001, 3)]
+
+
+@pytest.mark.parametrize("k,ops", FAST_CASES)
+@pytest.mark.parametrize("T", [1, 7, 32, 64])
+@pytest.mark.parametrize("path", ["k2", "k6", "slabs3"])
+def test_fast_mode_variants(h1, k, ops, T, path):
+    """Fast mode (scaled state, DESIGN.md c21) on every kernel family: K2 passes, K6 whole
+    solve, and the multi-slab schedule (K2 interior + K3 edges + exchange), incl. a tail pass."""
+    N = 300_001 if path != "k6" else 100_003
+    nt = 2 * T + 5
+    u0 = synth.uniform(int(k * 1000) + T, 0, N, -1.0, 1.0)
+    want = oracle.run(u0, k, nt)
+    kw = {"resident": False} if path == "k2" else {"resident": True} if path == "k6" else {"virtual_slabs": 3}
+    with h1.Heat1D(N, 1, nt, k, 1.0, 1.0, T=T, mode="fast", **kw) as h:
+        h.set_initial(u0)
+        assert h.info()["dp_ops"] == ops
+        h.run(nt)
+        got = h.get()
+    err = float(np.max(np.abs(got - want)))
+    assert err <= fast_bound(u0, nt), (k, T, path, err)
+
+
+def test_fast_mode_r_half_is_exact_average(h1):
+    """At r = 1/2 the scaled form is exactly u' = fl(u_{i-1} + u_{i+1}) / 2 per step (the
+    2^-T rescale is exact): check that sequence bitwise (numpy, no oracle arithmetic involved)."""
+    N, nt = 4099, 70
+    u0 = synth.uniform(3, 0, N, -1.0, 1.0)
+    want = u0.copy()
+    for _ in range(nt):
+        want = (np.roll(want, 1) + np.roll(want, -1)) * 0.5
+    for kw in ({"resident": False, "T": 32}, {"resident": True, "T": 32}, {"virtual_slabs": 2, "T": 9}):
+        with h1.Heat1D(N, 1, nt, 0.5, 1.0, 1.0, mode="fast", **kw) as h:
+            h.set_initial(u0)
+            h.run(nt)
+            assert_bitwise(h.get(), want, "r=1/2 fast %r" % kw)
+
+
+def test_fast_mode_range_fallback(h1):
+    """Values near the top of the fp64 range would overflow the scaled state (|u0| r^-T):
+    set_initial's K5 check falls back to the 3-op form, per initial state."""
+    N, nt = 50_000, 40
+    u0 = synth.uniform(6, 0, N, -1.0, 1.0)
+    big = u0 * 1e300
+    with h1.Heat1D(N, 1, nt, 0.25, 1.0, 1.0, T=32, mode="fast", resident=False) as h:
+        h.set_initial(big)
+        assert h.info()["dp_ops"] == 3
+        h.run(nt)
+        got = h.get()
+        assert np.all(np.isfinite(got))
+        assert np.max(np.abs(got - oracle.run(big, 0.25, nt))) <= fast_bound(big, nt)
+        h.set_initial(u0)                       # back in range: the scaled variant again
+        assert h.info()["dp_ops"] == 2
+        h.run(nt)
+        assert np.max(np.abs(h.get() - oracle.run(u0, 0.25, nt))) <= fast_bound(u0, nt)
+
+
+def test_fast_mode_c4_first_100_steps(h1):
+    """C4 at full size in fast mode (1 fp64 add per update): O3 windows at every slab
+    boundary, the wrap and random cells within the north_star bound."""
+    import torch
+    N, nt = C4.N, 100
+    r = oracle.r_of(C4.k, C4.dt, C4.dx)
+    out = torch.empty(N, dtype=torch.float64, device="cuda")
+    with h1.Heat1D(C4.nx, C4.np, nt, C4.k, C4.dt, C4.dx, mode="fast") as h:
+        h.init_uniform(C4.seed, C4.lo, C4.hi)
+        assert h.info()["dp_ops"] == 1
+        h.run()
+        h.get(out)
+    rng = np.random.default_rng(2)
+    for a in [g * C4.nx - 256 for g in range(8)] + list(rng.integers(0, N - 600, 8)):
+        idx = (np.arange(a, a + 512) % N).astype(np.int64)
+        got = out[torch.from_numpy(idx).cuda()].cpu().numpy()
+        w = oracle.window(C4.u0(a - nt, 512 + 2 * nt), nt, r)
+        assert np.max(np.abs(got - w)) <= 1e-12 * 1.0 * nt, a
+
+
+def test_fast_mode_c3_closed_form(h1):
+    """C3 at full size in fast mode (2 DP ops per update): the 8-mode closed form on a
+    strided sample, and O3 windows within the bound."""
+    import torch
+    N, nt = C3.N, C3.nt
+    r = oracle.r_of(C3.k, C3.dt, C3.dx)
+    u0 = C3.u0()
+    out = torch.empty(N, dtype=torch.float64, device="cuda")
+    with h1.Heat1D(C3.nx, C3.np, nt, C3.k, C3.dt, C3.dx, mode="fast") as h:
+        h.set_initial(u0)
+        assert h.info()["dp_ops"] == 2
+        h.run()
+        h.get(out)
+    got = out.cpu().numpy()
+    bound = fast_bound(u0, nt)
+    for a in [0, N - 64, C3.nx - 100, 12345677]:
+        w = oracle.window(C3.u0(a - nt, 512 + 2 * nt), nt, r)
+        assert np.max(np.abs(got[np.arange(a, a + 512) % N] - w)) <= bound, a
+    sel = np.arange(0, N, 101, dtype=np.int64)
+    want = np.zeros(sel.size)
+    for m, amp in zip(C3.modes, C3.amps()):
+        s_ = math.sin(math.pi * m / N)
+        want += amp * math.exp(nt * math.log1p(-4.0 * r * s_ * s_)) * np.sin(2.0 * np.pi * ((m * sel) % N) / N)
+    assert np.max(np.abs(got[sel] - want)) <= 1e-12 + bound
 
 
 def test_paper_2h_denominator(h1):
