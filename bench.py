@@ -199,9 +199,11 @@ def kernel_roofline(info, cfg, count, world, steps, k2_launches, k2_ms, ms, valu
     hbm_term = hbm / (16.0 / steps_per_pass)                 # GLUPS bound by HBM (BASELINE.json)
     fp64_term = FP64_TFLOPS * 1e3 / 4.0                      # GLUPS bound by FP64 peak / 4 flop
     bj_roof = min(hbm_term, fp64_term) * world
+    kind = info["pass_kind"]
     kernel = ("k6_resident<V=17>" if info["resident"] else
-              ["k2_pass", "k2w_pass", "k2p_pass"][info["pass_kind"]] + "<V=%d,NW=%d,S=%d>" % (
-                  info["pass_V"], info["pass_NW"], info["pass_S"])) + "<OPS=%d>" % info["dp_ops"]
+              ["k2_pass", "k2w_pass", "k2p_pass", "k2p_pass", "k2p_pass"][kind] + "<V=%d,NW=%d,S=%d%s>" % (
+                  info["pass_V"], info["pass_NW"], info["pass_S"],
+                  {3: ",KX=8", 4: ",KX=16"}.get(kind, ""))) + "<OPS=%d>" % info["dp_ops"]
     # the kernel's own bounds: HBM (16 B per cell per pass) and the fp64 pipe's issue rate
     # 148 SM x 64 lanes x 1.965 GHz against its algorithmic fp64 instructions per update
     # (dp_ops; the scaled fast variants add one rescale DMUL per cell per pass)

@@ -69,7 +69,7 @@ enum {
     HEAT1D_KERNEL_NAIVE = 1   /* one step per launch, modular indexing (K1; T forced to 1)    */
 };
 
-#define HEAT1D_T_MAX 64
+#define HEAT1D_T_MAX 128
 
 /* Options.  Always initialise with heat1d_opts_default(); `size` versions the struct. */
 typedef struct {

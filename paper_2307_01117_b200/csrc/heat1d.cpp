@@ -59,7 +59,7 @@ struct heat1d_s {
     int64_t steps_done = 0;
     int64_t launches = 0;
     int num_sms = 148;
-    PassGeom geom{33, 4, 3, 2, 2};
+    PassGeom geom{49, 4, 2, 2, 4};
     int last_grid = 0;
     bool resident = false;     // K6 path
     void *res_scratch = nullptr;
@@ -170,13 +170,13 @@ int64_t min_slab(int64_t nx, int64_t np, int32_t G) {
 }
 
 int auto_T(int ops) {
-    // DESIGN.md §6 (T sweeps in profiles/r01_tsweep_*.jsonl): each pass moves
-    // 16/T bytes per update, so T is raised until the pass is fp64-issue bound
-    // and the extra trapezoid work (2T/(32V) per warp) starts to cost more than
-    // the HBM power it frees under the 1 kW cap: 32 for the 3/4-op matched
-    // forms, 48 for the 2-op scaled form, 64 for the 1-op form at r = 1/2 (the
-    // only variant still HBM-bound at T = 32).
-    return ops == 1 ? 64 : ops == 2 ? 48 : 32;
+    // DESIGN.md §6 (T sweeps in profiles/r01_sweep_*.jsonl): each pass moves
+    // 16/T bytes per update, so T is raised until the pass is fp64-issue bound;
+    // with the inter-warp ghost exchange (kind 4) the extra work of a deeper
+    // pass is only the CTA-edge trapezoid 2T/(NW 32V), so T = 64 is at or
+    // within 1 % of the best measured T for all four arithmetic variants.
+    (void)ops;
+    return 64;
 }
 
 bool parse_geom_env(PassGeom *g) {

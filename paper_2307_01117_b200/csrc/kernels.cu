@@ -117,8 +117,9 @@ __device__ __forceinline__ void warp_step(const double (&u)[V], double (&v)[V], 
 
 // T steps in registers, ping-pong between u and a scratch array (no moves
 // inside the loop); the result is left in u.
-// Scaled variants (OPS <= 2) end the pass with u = v * r^T (`scale`, stencil.cuh).
-template <int V, int OPS>
+// Scaled variants (OPS <= 2) end the pass with u = v * r^T (`scale`, stencil.cuh),
+// unless RESCALE is false (a pass split into sub-periods rescales once at its end).
+template <int V, int OPS, bool RESCALE = true>
 __device__ __forceinline__ void warp_steps(double (&u)[V], int T, double r, double scale) {
     double v[V];
     int s = 0;
@@ -131,7 +132,7 @@ __device__ __forceinline__ void warp_steps(double (&u)[V], int T, double r, doub
 #pragma unroll
         for (int j = 0; j < V; ++j) u[j] = v[j];
     }
-    if constexpr (ops_scaled(OPS)) {
+    if constexpr (ops_scaled(OPS) && RESCALE) {
 #pragma unroll
         for (int j = 0; j < V; ++j) u[j] = __dmul_rn(u[j], scale);
     }
@@ -351,12 +352,22 @@ k2w_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
 // ------------------------------------------------------------------ K2 (warp-specialised)
 //
 // k2_pass with a dedicated producer warp: warps 0..NW-1 compute, warp NW owns
-// all TMA traffic.  The producer refills a stage as soon as the bulk store of
+// all TMA traffic.
+//
+// KX > 0 (kind 3): the compute warps of a CTA trade K-deep ghost zones through
+// shared memory every KX steps instead of each carrying a T-deep trapezoid --
+// PAPER.md:73's ghost exchange between neighbouring segments, at depth KX,
+// between warps.  Warp w holds tile-input cells [w(32V-2KX), w(32V-2KX)+32V);
+// after KX steps its KX outermost cells on an inner side are stale, and are
+// refreshed from the neighbour warp's first/last KX owned cells (lane 0 /
+// lane 31 registers; one named barrier per exchange, slots double-buffered by
+// parity).  Only the CTA's two outer sides keep the T-deep trapezoid, so the
+// redundant work falls from 2T/(32V) per warp to (2T + 2KX(NW-1))/(NW 32V).  The producer refills a stage as soon as the bulk store of
 // its previous tile has read it out, so S-1 loads are in flight while the
 // compute warps work; compute warps never wait for stores, and their only
 // CTA-level sync is a named barrier (B1) among themselves before the in-place
 // write-back.  Per stage: full[s] (TMA complete_tx) and done[s] (NW arrivals).
-template <int V, int NW, int S, int OPS>
+template <int V, int NW, int S, int OPS, int KX = 0>
 __global__ void __launch_bounds__((NW + 1) * 32)
 k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t out_lo,
          int64_t out_hi, int wrapT, double r, double scale, int64_t ntiles, uint32_t stage_doubles) {
@@ -368,9 +379,12 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform for the compiler
+    // KX == 0: warp spans of 32V overlapping by 2T; KX > 0: spans overlapping by 2KX
+    const int SW = KX > 0 ? 32 * V - 2 * KX : 32 * V - 2 * T;  // span stride
     const int OW = 32 * V - 2 * T;
-    const int64_t W = (int64_t)NW * OW;
+    const int64_t W = KX > 0 ? (int64_t)NW * 32 * V - 2 * KX * (NW - 1) - 2 * T : (int64_t)NW * OW;
     const int64_t stride = gridDim.x;
+    double *xbuf = stages + (size_t)S * stage_doubles;  // KX > 0: [2 parities][NW][2 sides][KX]
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
@@ -446,16 +460,56 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
         const int64_t x0 = out_lo + tile * W;
         const int sh = (int)((x0 - T) & 1);
         mbar_wait(&full[s], (uint32_t)((k / S) & 1));
-        const int base = sh + warp * OW + lane * V;
+        const int base = sh + warp * SW + lane * V;
         double u[V];
 #pragma unroll
         for (int j = 0; j < V; ++j) u[j] = st[base + j];
         asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");  // B1 among compute warps
-        warp_steps<V, OPS>(u, T, r, scale);
+        if constexpr (KX == 0) {
+            warp_steps<V, OPS>(u, T, r, scale);
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-            const int p = lane * V + j;
-            if (p >= T && p < 32 * V - T) st[base + j] = u[j];
+            for (int j = 0; j < V; ++j) {
+                const int p = lane * V + j;
+                if (p >= T && p < 32 * V - T) st[base + j] = u[j];
+            }
+        } else {
+            int dn = 0;
+            for (int e = 0;; ++e) {
+                const int Ks = (T - dn) < KX ? (T - dn) : KX;
+                warp_steps<V, OPS, false>(u, Ks, r, 1.0);  // (rescale below, once per pass)
+                dn += Ks;
+                if (dn >= T) break;
+                double *X = xbuf + (size_t)(e & 1) * (NW * 2 * KX);
+                if (lane == 0 && warp > 0) {
+#pragma unroll
+                    for (int i = 0; i < KX; ++i) X[(warp * 2 + 0) * KX + i] = u[KX + i];
+                }
+                if (lane == 31 && warp < NW - 1) {
+#pragma unroll
+                    for (int i = 0; i < KX; ++i) X[(warp * 2 + 1) * KX + i] = u[V - 2 * KX + i];
+                }
+                asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+                if (lane == 0 && warp > 0) {
+#pragma unroll
+                    for (int i = 0; i < KX; ++i) u[i] = X[((warp - 1) * 2 + 1) * KX + i];
+                }
+                if (lane == 31 && warp < NW - 1) {
+#pragma unroll
+                    for (int i = 0; i < KX; ++i) u[V - KX + i] = X[((warp + 1) * 2 + 0) * KX + i];
+                }
+            }
+            if constexpr (ops_scaled(OPS)) {
+#pragma unroll
+                for (int j = 0; j < V; ++j) u[j] = __dmul_rn(u[j], scale);
+            }
+            // owned cells: inner sides exclude the KX ghost zone, the CTA's outer sides the T-deep one
+            const int lo = warp == 0 ? T : KX;
+            const int hi = warp == NW - 1 ? 32 * V - T : 32 * V - KX;
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                const int p = lane * V + j;
+                if (p >= lo && p < hi) st[base + j] = u[j];
+            }
         }
         fence_proxy_async();
         __syncwarp();
@@ -464,10 +518,11 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
 }
 
 size_t PassGeom::smem_bytes(int T) const {
-    if (kind == 0 || kind == 2) {
+    if (kind != 1) {
         const int64_t in_cells = tile_out(T) + 2 * T + 2;
         const int64_t stage = (in_cells + 15) / 16 * 16;
-        return 128 + (size_t)S * (size_t)stage * sizeof(double);
+        const size_t xch = (size_t)2 * NW * 2 * kx_of(kind) * sizeof(double);
+        return 128 + (size_t)S * (size_t)stage * sizeof(double) + xch;
     }
     const int64_t slot = (32 * (int64_t)V + 2 + 15) / 16 * 16;
     const size_t bar = (size_t)((NW * S * 8 + 127) / 128) * 128;
@@ -484,6 +539,19 @@ PassFn pass_fn(int kind) {
     return kind == 0 ? &k2_pass<V, NW, S, OPS> : kind == 1 ? &k2w_pass<V, NW, S, OPS> : &k2p_pass<V, NW, S, OPS>;
 }
 
+// kinds 3 and 4 (inter-warp ghost exchange) for all four arithmetic variants
+#define HEAT1D_GEOMS_X(X) X(17, 4, 3) X(17, 8, 3) X(25, 4, 3) X(33, 4, 3) X(33, 8, 2) X(33, 8, 3) X(41, 4, 2) X(49, 4, 2) X(49, 8, 2) X(53, 4, 2) X(65, 4, 2)
+
+template <int V, int NW, int S, int KX>
+PassFn pass_fn_x(int ops) {
+    switch (ops) {
+        case 4: return &k2p_pass<V, NW, S, 4, KX>;
+        case 3: return &k2p_pass<V, NW, S, 3, KX>;
+        case 2: return &k2p_pass<V, NW, S, 2, KX>;
+        default: return &k2p_pass<V, NW, S, 1, KX>;
+    }
+}
+
 // (V, NW, S) instantiated for all three kernel kinds and both arithmetic variants:
 // the defaults plus the tuning points the sweeps and tests use.
 #define HEAT1D_GEOMS(X)                                                                            \
@@ -496,6 +564,13 @@ PassFn pass_fn(int kind) {
 #define HEAT1D_GEOMS_SCALED(X) X(9, 4, 3) X(17, 8, 3) X(25, 4, 3) X(33, 4, 3) X(33, 8, 3) X(49, 4, 3)
 
 PassFn lookup_pass(int V, int NW, int S, int ops, int kind) {
+    if (kind == 3 || kind == 4) {
+#define X(v, nw, s) \
+    if (V == v && NW == nw && S == s) return kind == 3 ? pass_fn_x<v, nw, s, 8>(ops) : pass_fn_x<v, nw, s, 16>(ops);
+        HEAT1D_GEOMS_X(X)
+#undef X
+        return nullptr;
+    }
     if (ops == 4 || ops == 3) {
 #define X(v, nw, s)                                                                                \
     if (V == v && NW == nw && S == s)                                                              \
@@ -515,12 +590,12 @@ PassFn lookup_pass(int V, int NW, int S, int ops, int kind) {
 }  // namespace
 
 PassGeom choose_geom(int64_t n_out, int T, int num_sms) {
-    // Default (profiles/r01_sweeps.jsonl): CTA tiles of 4 compute
-    // warps x V=33 cells/lane plus a TMA producer warp, 3 stages (~102 KB),
-    // 2 CTAs per SM.  Rings too small to give every CTA a tile use 4-warp
-    // tiles of V=9.
-    PassGeom g{33, 4, 3, 2, 2};
-    if (n_out < (int64_t)num_sms * g.ctas_per_sm * g.tile_out(T)) g = PassGeom{9, 4, 3, 4, 2};
+    // Default (profiles/r01_sweep_kx.jsonl): CTA tiles of 4 compute
+    // warps x V=49 cells/lane trading 16-deep ghosts every 16 steps (kind 4),
+    // plus a TMA producer warp, 2 stages (~101 KB), 2 CTAs per SM.  Rings too
+    // small to give every CTA a tile use 4-warp V=17 tiles exchanging every 8 steps.
+    PassGeom g{49, 4, 2, 2, 4};
+    if (n_out < (int64_t)num_sms * g.ctas_per_sm * g.tile_out(T)) g = PassGeom{17, 4, 3, 4, 3};
     return g;
 }
 
@@ -534,7 +609,11 @@ cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, 
         return cudaSuccess;
     }
     const int64_t W = g.tile_out(T);
-    if (W <= 0 || 32 * g.V - 2 * T <= 0) return cudaErrorInvalidValue;
+    const int kx = kx_of(g.kind);
+    if (W <= 0 || (!kx && 32 * g.V - 2 * T <= 0)) return cudaErrorInvalidValue;
+    // kinds 3, 4: the outer warps' T-deep trapezoid must stay inside their span, and the
+    // exchanged KX-cell edges inside one lane
+    if (kx && (T > 32 * g.V - kx || g.V < 2 * kx)) return cudaErrorInvalidValue;
     const int64_t units = (out_hi - out_lo + W - 1) / W;
     const size_t smem = g.smem_bytes(T);
     const int64_t in_cells = (g.kind != 1 ? W : 32 * (int64_t)g.V - 2 * T) + 2 * T + 2;
@@ -561,7 +640,7 @@ cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, 
     // Persistent grid: never more CTAs than can be co-resident (static round-robin
     // assignment assumes a single wave).
     int occ = 0;
-    const int threads = (g.NW + (g.kind == 2 ? 1 : 0)) * 32;
+    const int threads = (g.NW + (g.kind >= 2 ? 1 : 0)) * 32;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)fn, threads, smem) != cudaSuccess ||
         occ < 1)
         occ = 1;
@@ -602,7 +681,7 @@ cudaError_t launch_naive(int ops, const double *A, double *B, int64_t n, double 
 template <int OPS>
 __global__ void __launch_bounds__(96) k3_edges(const double *__restrict__ A, double *__restrict__ B, int64_t n,
                                                int T, double r, double scale) {
-    __shared__ double w[2][3 * 64];
+    __shared__ double w[2][3 * 128];
     const int64_t base = (blockIdx.x == 0) ? -(int64_t)T : n - 2 * (int64_t)T;
     const int len = 3 * T;
     for (int i = threadIdx.x; i < len; i += blockDim.x) w[0][i] = A[base + i];
@@ -624,7 +703,7 @@ __global__ void __launch_bounds__(96) k3_edges(const double *__restrict__ A, dou
 
 cudaError_t launch_edges(int ops, const double *A, double *B, int64_t n, int T, double q, double scale,
                          cudaStream_t st) {
-    if (T < 1 || T > 64) return cudaErrorInvalidValue;
+    if (T < 1 || T > 128) return cudaErrorInvalidValue;
     switch (ops) {
         case 4: k3_edges<4><<<2, 96, 0, st>>>(A, B, n, T, q, scale); break;
         case 3: k3_edges<3><<<2, 96, 0, st>>>(A, B, n, T, q, scale); break;

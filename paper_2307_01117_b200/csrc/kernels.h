@@ -21,6 +21,10 @@ __host__ __device__ inline double scale_of(double r, int Tp) {
 }
 
 
+// Ghost depth (= steps between exchanges) of the inter-warp exchange of pass-kernel
+// kinds 3 (8) and 4 (16); 0 for the other kinds.
+constexpr int kx_of(int kind) { return kind == 3 ? 8 : kind == 4 ? 16 : 0; }
+
 // Geometry of the temporal-blocked pass kernel (K2) for one launch config.
 struct PassGeom {
     int V;            // cells per thread (odd: conflict-free 64-bit LDS/STS)
@@ -30,9 +34,15 @@ struct PassGeom {
     int kind = 1;     // 0: CTA tiles (one TMA copy per CTA tile, 2 CTA barriers per tile)
                       // 1: warp-autonomous spans (each warp its own TMA ring; no CTA barriers)
                       // 2: CTA tiles + a dedicated TMA producer warp (NW+1 warps per CTA)
+                      // 3, 4: kind 2 + compute warps trade kx_of(kind)-deep ghosts through
+                      //    shared memory every kx_of(kind) steps (only the CTA edges keep the
+                      //    T trapezoid)
     size_t smem_bytes(int T) const;
     // output cells per scheduling unit (a CTA tile for kind 0, a warp span for kind 1)
-    int64_t tile_out(int T) const { return (kind != 1 ? (int64_t)NW : 1) * (32 * V - 2 * T); }
+    int64_t tile_out(int T) const {
+        if (kx_of(kind)) return (int64_t)NW * 32 * V - 2 * (int64_t)kx_of(kind) * (NW - 1) - 2 * T;
+        return (kind != 1 ? (int64_t)NW : 1) * (32 * V - 2 * T);
+    }
 };
 
 // Pick the pass-kernel configuration for (n, T).

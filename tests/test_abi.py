@@ -104,7 +104,7 @@ def test_create_validation_without_gpu(lib, args, status):
 
 def test_bad_opts(lib):
     import paper_2307_01117_b200 as h1
-    for kw, st in [(dict(T=65), 1), (dict(T=-1), 1), (dict(rank=2, nranks=2), 1), (dict(nranks=2), 1),
+    for kw, st in [(dict(T=129), 1), (dict(T=-1), 1), (dict(rank=2, nranks=2), 1), (dict(nranks=2), 1),
                    (dict(virtual_slabs=0), 1), (dict(virtual_slabs=2, kernel="naive"), 7)]:
         with pytest.raises(h1.Heat1DError) as ei:
             h1.Heat1D(100, 4, 10, 0.25, 1.0, 1.0, **kw)

@@ -44,7 +44,7 @@ def assert_bitwise(got, want, what=""):
 
 
 # ------------------------------------------------------------------ C1
-@pytest.mark.parametrize("T", [0, 1, 2, 3, 4, 5, 8, 12, 16, 31, 32, 33, 48, 64])
+@pytest.mark.parametrize("T", [0, 1, 2, 3, 4, 5, 8, 12, 16, 31, 32, 33, 48, 64, 100, 128])
 def test_c1_bitwise_all_T(h1, T):
     r = oracle.r_of(C1.k, C1.dt, C1.dx)
     want = oracle.run(C1.u0(), r, C1.nt)
@@ -129,7 +129,9 @@ def test_resident_refuses_too_large(h1):
                                   "9,4,3,4,1", "9,8,4,2,1", "17,4,2,4,1", "17,8,3,2,1", "17,8,2,2,1",
                                   "21,8,3,1,1", "25,4,3,2,1", "25,8,2,1,1", "33,4,2,2,1", "33,8,2,1,1",
                                   "9,4,3,4,2", "17,8,3,2,2", "17,8,4,1,2", "17,8,2,3,2", "17,4,4,3,2",
-                                  "25,4,3,2,2", "33,4,3,2,2", "15,8,3,2,2", "17,16,2,1,2"])
+                                  "25,4,3,2,2", "33,4,3,2,2", "15,8,3,2,2", "17,16,2,1,2",
+                                  "17,8,3,2,3", "25,4,3,2,3", "33,4,3,2,3", "33,8,2,1,3",
+                                  "33,8,3,1,3", "49,4,2,2,3", "33,4,3,2,4", "33,8,2,1,4", "49,4,2,2,4"])
 def test_all_pass_geometries(h1, geom, monkeypatch):
     monkeypatch.setenv("HEAT1D_GEOM", geom)
     N, nt = 300_001, 29
@@ -137,6 +139,23 @@ def test_all_pass_geometries(h1, geom, monkeypatch):
     for k, T in [(0.4, 7), (0.5, 12)]:
         want = oracle.run(u0, k, nt)
         assert_bitwise(gpu_run(h1, u0, N, 1, nt, k, T=T, resident=False), want, "geom %s T=%d" % (geom, T))
+
+
+@pytest.mark.parametrize("geom", ["33,4,3,2,3", "17,8,3,2,3", "49,4,2,2,3", "33,4,3,2,4", "49,4,2,2,4"])
+@pytest.mark.parametrize("T", [1, 2, 7, 8, 9, 16, 17, 32, 64, 96, 128])
+def test_interwarp_exchange_kernel(h1, geom, T, monkeypatch):
+    """Pass kind 3 (ghost exchange between the warps of a CTA every 8 steps): T below,
+    at and between multiples of the exchange depth, matched 4-op / 3-op and both fast
+    variants, incl. tail passes and ragged tiles."""
+    monkeypatch.setenv("HEAT1D_GEOM", geom)
+    N = 200_003
+    nt = 2 * T + 3
+    u0 = synth.uniform(1000 + T, 0, N, -1.0, 1.0)
+    for k in (0.4, 0.5):
+        want = oracle.run(u0, k, nt)
+        assert_bitwise(gpu_run(h1, u0, N, 1, nt, k, T=T, resident=False), want, "kind3 %s T=%d k=%g" % (geom, T, k))
+        got = gpu_run(h1, u0, N, 1, nt, k, T=T, resident=False, mode="fast")
+        assert np.max(np.abs(got - want)) <= fast_bound(u0, nt)
 
 
 # ------------------------------------------------------------------ C2 (paper's workload size)
@@ -167,7 +186,7 @@ def test_cross_T_bitwise(h1):
     for T in [1, 2, 3, 4, 6, 8, 11, 12, 16, 24, 32]:
         for res in (False, True):
             assert_bitwise(gpu_run(h1, u0, N, 1, nt, 0.4, T=T, resident=res), ref, "T=%d res=%s" % (T, res))
-    for T in [33, 40, 48, 63, 64]:
+    for T in [33, 40, 48, 63, 64, 96, 128]:
         assert_bitwise(gpu_run(h1, u0, N, 1, nt, 0.4, T=T, resident=False), ref, "T=%d" % T)
 
 
