@@ -59,6 +59,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     }
 }
 
+// Same, but the waiting thread is suspended in hardware until the phase completes (or the
+// time hint, in ns, runs out) instead of re-issuing try_wait: a waiting warp then takes no
+// issue slots from the compute warps sharing its SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+            : "memory");
+    } while (!ok);
+}
+
 // TMA 1D bulk copy global -> shared, completion counted on an mbarrier (SASS: UBLKCP).
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
                                          uint64_t policy) {
@@ -117,6 +133,19 @@ __device__ __forceinline__ void warp_step(const double (&u)[V], double (&v)[V], 
 
 // T steps in registers, ping-pong between u and a scratch array (no moves
 // inside the loop); the result is left in u.
+// N (even, compile time) steps fully unrolled: the sub-periods of the exchanging
+// pass kinds, with no loop control between steps.
+template <int V, int OPS, int N>
+__device__ __forceinline__ void warp_steps_fixed(double (&u)[V], double r) {
+    static_assert(N % 2 == 0, "even step count keeps the result in u");
+    double v[V];
+#pragma unroll
+    for (int s = 0; s < N; s += 2) {
+        warp_step<V, OPS>(u, v, r);
+        warp_step<V, OPS>(v, u, r);
+    }
+}
+
 // Scaled variants (OPS <= 2) end the pass with u = v * r^T (`scale`, stencil.cuh),
 // unless RESCALE is false (a pass split into sub-periods rescales once at its end).
 template <int V, int OPS, bool RESCALE = true>
@@ -424,7 +453,7 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
             const int64_t x1 = min(x0 + W, out_hi);
             const int64_t lo = x0 - T;
             const int64_t ld_lo = lo - (lo & 1);
-            mbar_wait(&done[s], (uint32_t)((k / S) & 1));
+            mbar_wait_sleep(&done[s], (uint32_t)((k / S) & 1));
             // scalar leftovers: an odd first/last cell and the periodic self-halo
             if (lane == 0 && (x0 & 1)) B[x0] = st[x0 - ld_lo];
             if (lane == 1 && (x1 & 1) && x1 - 1 >= x0) B[x1 - 1] = st[x1 - 1 - ld_lo];
@@ -459,7 +488,7 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
         double *st = stages + (size_t)s * stage_doubles;
         const int64_t x0 = out_lo + tile * W;
         const int sh = (int)((x0 - T) & 1);
-        mbar_wait(&full[s], (uint32_t)((k / S) & 1));
+        mbar_wait_sleep(&full[s], (uint32_t)((k / S) & 1));
         const int base = sh + warp * SW + lane * V;
         double u[V];
 #pragma unroll
@@ -476,7 +505,12 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
             int dn = 0;
             for (int e = 0;; ++e) {
                 const int Ks = (T - dn) < KX ? (T - dn) : KX;
-                warp_steps<V, OPS, false>(u, Ks, r, 1.0);  // (rescale below, once per pass)
+                // (full unrolling pays for the 1-op form only: the 3/4-op sub-period
+                // code would outgrow the instruction cache)
+                if (OPS == 1 && Ks == KX)
+                    warp_steps_fixed<V, OPS, KX>(u, r);
+                else
+                    warp_steps<V, OPS, false>(u, Ks, r, 1.0);  // (rescale below, once per pass)
                 dn += Ks;
                 if (dn >= T) break;
                 double *X = xbuf + (size_t)(e & 1) * (NW * 2 * KX);
