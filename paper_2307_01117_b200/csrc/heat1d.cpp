@@ -589,7 +589,9 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     const bool res_ok = (G == 1 && o.kernel == HEAT1D_KERNEL_AUTO && o.resident != 0);
     if (res_ok) {
         const int64_t n0 = h->N;
-        int Tr = (o.T > 0 && o.T < 32) ? o.T : 32;  // K6 period: halo refresh every <= 32 steps (one lane per halo cell)
+        // K6 period (halo refresh) <= 64; auto = 64 (V = 33 spans): half the exchanges of T = 32
+        // for +32 % (C5) / +30 % (C2) measured (profiles/r01_k6_period_sync.jsonl)
+        int Tr = (o.T > 0 && o.T < 64) ? o.T : 64;
         if (Tr > n0) Tr = (int)n0;
         int coop = 0;
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);

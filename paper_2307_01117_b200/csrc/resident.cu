@@ -143,9 +143,9 @@ __device__ __forceinline__ void regs_to_row(const double (&u)[V], double *row, i
 __device__ __forceinline__ void publish(const Span &s, int T, unsigned p, double *edges, unsigned *flags,
                                         int lane) {
     double *E = edges + ((size_t)s.id * 4 + (p & 1) * 2) * T;
-    if (lane < T) {                         // T <= 32
-        E[lane] = s.row[T + lane];          // side 0: first T owned cells
-        E[T + lane] = s.row[s.own + lane];  // side 1: last T owned cells
+    for (int i = lane; i < T; i += 32) {
+        E[i] = s.row[T + i];          // side 0: first T owned cells
+        E[T + i] = s.row[s.own + i];  // side 1: last T owned cells
     }
     __syncwarp();  // orders the lanes' writes before lane 0's (cumulative) release
     if (lane == 0) st_release(flags + s.id, p + 1);
@@ -153,21 +153,32 @@ __device__ __forceinline__ void publish(const Span &s, int T, unsigned p, double
 
 // wait for the neighbours' period-p edges and write them into the halos
 __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, const double *edges,
-                                        const unsigned *flags, int lane) {
+                                        const unsigned *flags, int lane, int sync) {
     // every lane polls (one coalesced request per poll); the vote makes the exit
     // warp-uniform, so ptxas keeps the step loop's shuffles non-collective.
     // Relaxed polls: an acquire at gpu scope invalidates L1 (CCTL.IVALL) each
     // time; one acquire per flag after the wait orders the edge reads.
-    while (!__all_sync(0xffffffffu, ld_relaxed(flags + s.left) >= p + 1 && ld_relaxed(flags + s.right) >= p + 1)) {
+    // sync 0: relaxed polls, then one acquire per flag; 1: acquire polls; 2: relaxed polls,
+    // then one fence (the PTX acquire pattern); tuning knob HEAT1D_K6_SYNC.
+    if (sync == 1) {
+        while (!__all_sync(0xffffffffu, ld_acquire(flags + s.left) >= p + 1 && ld_acquire(flags + s.right) >= p + 1)) {
+        }
+    } else {
+        while (!__all_sync(0xffffffffu, ld_relaxed(flags + s.left) >= p + 1 && ld_relaxed(flags + s.right) >= p + 1)) {
+        }
+        if (sync == 2) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        } else {
+            (void)ld_acquire(flags + s.left);
+            (void)ld_acquire(flags + s.right);
+        }
     }
-    (void)ld_acquire(flags + s.left);
-    (void)ld_acquire(flags + s.right);
     __syncwarp();
     const double *LE = edges + ((size_t)s.left * 4 + (p & 1) * 2) * T + T;  // left's side 1
     const double *RE = edges + ((size_t)s.right * 4 + (p & 1) * 2) * T;     // right's side 0
-    if (lane < T) {
-        s.row[lane] = __ldcg(LE + lane);
-        s.row[s.own + T + lane] = __ldcg(RE + lane);
+    for (int i = lane; i < T; i += 32) {
+        s.row[i] = __ldcg(LE + i);
+        s.row[s.own + T + i] = __ldcg(RE + i);
     }
     __syncwarp();
 }
@@ -177,7 +188,7 @@ __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, const 
 template <int V, int OPS, int SPW, bool EARLY>
 __global__ void __launch_bounds__(256)
 k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t nt, double r,
-            double rr, double *__restrict__ edges, unsigned *__restrict__ flags, int Wt) {
+            double rr, double *__restrict__ edges, unsigned *__restrict__ flags, int Wt, int sync) {
     extern __shared__ __align__(16) double srow[];
     const int lane = threadIdx.x & 31;
     const int wib = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);  // warp-uniform for the compiler
@@ -202,7 +213,7 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
             done += Tp;
             if (done >= nt) break;
             publish(a, T, p, edges, flags, lane);
-            refresh(a, T, p, edges, flags, lane);
+            refresh(a, T, p, edges, flags, lane, sync);
             row_to_regs<V>(a.row, ua, lane);
         }
 #pragma unroll
@@ -224,7 +235,7 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
             regs_to_row<V>(ua, a.row, lane);
             if (!last) publish(a, T, p, edges, flags, lane);
             if (p > 0) {  // B's halos for period p: neighbours' period p-1 edges
-                refresh(b, T, p - 1, edges, flags, lane);
+                refresh(b, T, p - 1, edges, flags, lane, sync);
                 row_to_regs<V>(b.row, ub, lane);
             }
             steps_regs<V, OPS, EARLY>(ub, v, Tp, r, sc);
@@ -232,7 +243,7 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
             if (!last) publish(b, T, p, edges, flags, lane);
             done += Tp;
             if (last) break;
-            refresh(a, T, p, edges, flags, lane);  // overlapped with B's compute above
+            refresh(a, T, p, edges, flags, lane, sync);  // overlapped with B's compute above
             row_to_regs<V>(a.row, ua, lane);
         }
 #pragma unroll
@@ -245,15 +256,17 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
 }
 
 namespace {
-constexpr int RV = 17;        // cells per lane
-// warps per SM the register budget allows: ~100 regs (1 span/warp), ~156 (2 spans/warp)
-constexpr int MAX_WPS1 = 20, MAX_WPS2 = 12;
-constexpr int MAX_WPS = MAX_WPS1;
+// cells per lane: 17 for periods T <= 32, 33 for 32 < T <= 64 (span 32V >= own + 2T)
+int rv_of(int T) { return T > 32 ? 33 : 17; }
+// warps per SM the register budget allows: V=17: ~100 regs (1 span/warp), ~156 (2 spans/warp);
+// V=33: ~128 regs (1 span/warp only)
+int max_wps(int rv, int spw) { return rv == 33 ? 15 : spw == 1 ? 20 : 12; }
+constexpr int MAX_WPS_ANY = 20;
 constexpr int MAX_NW = 8;     // warps per CTA (__launch_bounds__(256))
 
 struct ResPlan {
     int64_t wt = 0, nw = 0, grid = 0;
-    int spw = 2;
+    int spw = 2, rv = 17;
     size_t smem = 0;
 };
 
@@ -262,22 +275,28 @@ int res_early() {
     return e ? atoi(e) : 1;
 }
 
-const void *res_fn(int ops, int spw) {
+int res_sync() {
+    const char *e = getenv("HEAT1D_K6_SYNC");  // tuning knob (refresh's acquire pattern)
+    return e ? atoi(e) : 0;
+}
+
+const void *res_fn(int ops, int spw, int rv) {
     const bool early = res_early() != 0;
-#define RF(o, s, e) (const void *)&k6_resident<RV, o, s, e>
-#define RF_OPS(s, e) (ops == 4 ? RF(4, s, e) : ops == 3 ? RF(3, s, e) : ops == 2 ? RF(2, s, e) : RF(1, s, e))
-    if (spw == 1) return early ? RF_OPS(1, true) : RF_OPS(1, false);
-    return early ? RF_OPS(2, true) : RF_OPS(2, false);
+#define RF(v, o, s, e) (const void *)&k6_resident<v, o, s, e>
+#define RF_OPS(v, s, e) (ops == 4 ? RF(v, 4, s, e) : ops == 3 ? RF(v, 3, s, e) : ops == 2 ? RF(v, 2, s, e) : RF(v, 1, s, e))
+    if (rv == 33) return early ? RF_OPS(33, 1, true) : RF_OPS(33, 1, false);
+    if (spw == 1) return early ? RF_OPS(17, 1, true) : RF_OPS(17, 1, false);
+    return early ? RF_OPS(17, 2, true) : RF_OPS(17, 2, false);
 #undef RF_OPS
 #undef RF
 }
 
 cudaError_t res_attr(const void *fn) {
-    static const void *done[16] = {nullptr};
+    static const void *done[32] = {nullptr};
     for (const void *d : done)
         if (d == fn) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         2 * 16 * (32 * RV + 1) * 8);
+                                         2 * 16 * (32 * 17 + 1) * 8);  // >= 8 warps x (32*33+1) too
     if (e != cudaSuccess) return e;
     for (auto &d : done)
         if (!d) {
@@ -290,12 +309,14 @@ cudaError_t res_attr(const void *fn) {
 // Split the ring into Ns = spw*Wt equal spans (each owning >= T cells, span
 // own + 2T <= 32*RV) with warps balanced across SMs.
 bool res_plan(int ops, int64_t n, int T, int num_sms, ResPlan *p) {
+    const int RV = rv_of(T);
+    p->rv = RV;
     const int cap = 32 * RV - 2 * T;
     if (T < 1 || cap <= 0 || n < T) return false;
     // 1 span per warp by default (profiles/r01_k6_ab_*.jsonl: 2 spans per warp do
     // not pay on B200); HEAT1D_K6_SPW=2 selects the alternating two-span warps.
     p->spw = 1;
-    if (const char *e = getenv("HEAT1D_K6_SPW")) p->spw = (atoi(e) == 2 && n >= 2 * (int64_t)T) ? 2 : 1;
+    if (const char *e = getenv("HEAT1D_K6_SPW")) p->spw = (atoi(e) == 2 && n >= 2 * (int64_t)T && RV == 17) ? 2 : 1;
     const int64_t ns_min = (n + cap - 1) / cap;
     const int64_t wt_min = (ns_min + p->spw - 1) / p->spw;
     if (wt_min <= num_sms) {
@@ -304,7 +325,7 @@ bool res_plan(int ops, int64_t n, int T, int num_sms, ResPlan *p) {
         p->grid = p->wt;
     } else {
         const int64_t wps = (wt_min + num_sms - 1) / num_sms;
-        if (wps > (p->spw == 1 ? MAX_WPS1 : MAX_WPS2)) return false;
+        if (wps > max_wps(RV, p->spw)) return false;
         const int64_t cps = (wps + MAX_NW - 1) / MAX_NW;  // CTAs per SM (blocks <= 8 warps)
         p->nw = (wps + cps - 1) / cps;
         p->grid = (int64_t)num_sms * cps;
@@ -318,7 +339,7 @@ bool res_plan(int ops, int64_t n, int T, int num_sms, ResPlan *p) {
     const int64_t ns = p->wt * p->spw;
     if (n / ns < T || n / ns + (n % ns ? 1 : 0) + 2 * T > 32 * RV) return false;
     p->smem = (size_t)p->nw * p->spw * (32 * RV + 1) * sizeof(double);
-    const void *fn = res_fn(ops, p->spw);
+    const void *fn = res_fn(ops, p->spw, RV);
     if (res_attr(fn) != cudaSuccess) return false;
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, (int)(p->nw * 32), p->smem) != cudaSuccess)
@@ -329,8 +350,9 @@ bool res_plan(int ops, int64_t n, int T, int num_sms, ResPlan *p) {
 }  // namespace
 
 int64_t resident_capacity(int T, int num_sms) {
-    const int64_t a = (int64_t)MAX_WPS1, b = 2 * (int64_t)MAX_WPS2;
-    return (int64_t)num_sms * (a > b ? a : b) * (32 * RV - 2 * T);
+    const int rv = rv_of(T);
+    const int64_t a = max_wps(rv, 1), b = rv == 17 ? 2 * (int64_t)max_wps(rv, 2) : 0;
+    return (int64_t)num_sms * (a > b ? a : b) * (32 * rv - 2 * T);
 }
 
 bool resident_fits(int ops, int64_t n, int T, int num_sms) {
@@ -339,7 +361,7 @@ bool resident_fits(int ops, int64_t n, int T, int num_sms) {
 }
 
 size_t resident_scratch_bytes(int T, int num_sms) {
-    const int64_t ns = (int64_t)num_sms * (MAX_WPS1 > 2 * MAX_WPS2 ? MAX_WPS1 : 2 * MAX_WPS2);
+    const int64_t ns = (int64_t)num_sms * 2 * MAX_WPS_ANY;
     return (size_t)ns * 4 * T * sizeof(double) + (size_t)ns * sizeof(unsigned) + 256;
 }
 
@@ -353,13 +375,14 @@ cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int 
     cudaError_t e = cudaMemsetAsync(flags, 0, (size_t)ns * sizeof(unsigned), st);
     if (e != cudaSuccess) return e;
     int Wt = (int)p.wt;
+    int sync = res_sync();
     void *args[] = {(void *)&A, (void *)&B, (void *)&n, (void *)&T, (void *)&nt, (void *)&q, (void *)&r,
-                    (void *)&edges, (void *)&flags, (void *)&Wt};
+                    (void *)&edges, (void *)&flags, (void *)&Wt, (void *)&sync};
     if (warps_out) *warps_out = Wt;
     if (getenv("HEAT1D_DEBUG"))
         fprintf(stderr, "[heat1d] K6 n=%lld T=%d spw=%d Wt=%d nw=%lld grid=%lld smem=%zu\n", (long long)n, T,
                 p.spw, Wt, (long long)p.nw, (long long)p.grid, p.smem);
-    return cudaLaunchCooperativeKernel(res_fn(ops, p.spw), dim3((unsigned)p.grid), dim3((unsigned)(p.nw * 32)),
+    return cudaLaunchCooperativeKernel(res_fn(ops, p.spw, p.rv), dim3((unsigned)p.grid), dim3((unsigned)(p.nw * 32)),
                                        args, p.smem, st);
 }
 

@@ -87,7 +87,7 @@ def test_ragged_multi_tile(h1, N, T, k, resident):
 
 
 @pytest.mark.parametrize("N", [1, 2, 7, 33, 544, 545, 5000, 80_000, 1_000_000, 1_400_000])
-@pytest.mark.parametrize("T", [1, 5, 16, 32])
+@pytest.mark.parametrize("T", [1, 5, 16, 32, 33, 64])
 def test_resident_kernel(h1, N, T):
     """K6 (whole solve in one cooperative launch, slab in registers) vs the oracle:
     one warp, a few warps, one warp per SM, many warps per SM, near capacity."""
@@ -116,6 +116,19 @@ def test_resident_two_span_warps(h1, monkeypatch, early):
             h.set_initial(u0)
             h.run()
             assert_bitwise(h.get(), oracle.run(u0, 0.5, nt), "K6 spw=2 N=%d" % N)
+
+
+@pytest.mark.parametrize("sync", ["0", "1", "2"])
+def test_resident_sync_variants(h1, monkeypatch, sync):
+    """K6's three acquire patterns for the halo refresh (tuning knob HEAT1D_K6_SYNC)."""
+    monkeypatch.setenv("HEAT1D_K6_SYNC", sync)
+    for N, T in [(100_003, 32), (1 << 20, 64)]:
+        nt = 3 * T + 1
+        u0 = synth.uniform(N + 1, 0, N, -1.0, 1.0)
+        with h1.Heat1D(N, 1, nt, 0.4, 1.0, 1.0, T=T, resident=True) as h:
+            h.set_initial(u0)
+            h.run()
+            assert_bitwise(h.get(), oracle.run(u0, 0.4, nt), "K6 sync=%s N=%d" % (sync, N))
 
 
 def test_resident_refuses_too_large(h1):
