@@ -505,3 +505,28 @@ def test_c4_first_100_steps_windows(h1):
         out2 = torch.empty(N, dtype=torch.float64, device="cuda")
         h.get(out2)
     assert torch.equal(out, out2)
+
+
+@pytest.mark.parametrize("mode", ["matched", "fast"])
+def test_c4_full_nt_windows(h1, mode):
+    """C4 exactly as bench.py times it (2^31 cells, all 10,000 steps, default T and kernels):
+    O3 light-cone windows of the FINAL field at slab boundaries, the wrap and random cells --
+    bitwise (matched) or within the north_star bound (fast)."""
+    import torch
+    N, nt = C4.N, C4.nt
+    r = oracle.r_of(C4.k, C4.dt, C4.dx)
+    out = torch.empty(N, dtype=torch.float64, device="cuda")
+    with h1.Heat1D(C4.nx, C4.np, nt, C4.k, C4.dt, C4.dx, mode=mode) as h:
+        h.init_uniform(C4.seed, C4.lo, C4.hi)
+        h.run()
+        h.get(out)
+    rng = np.random.default_rng(3)
+    W = 256
+    for a in [0, N - W // 2, 3 * C4.nx - W // 2] + list(rng.integers(0, N - W, 3)):
+        idx = (np.arange(a, a + W) % N).astype(np.int64)
+        got = out[torch.from_numpy(idx).cuda()].cpu().numpy()
+        w = oracle.window(C4.u0(a - nt, W + 2 * nt), nt, r)
+        if mode == "matched":
+            assert_bitwise(got, w, "C4 nt=10000 window %d" % a)
+        else:
+            assert np.max(np.abs(got - w)) <= 1e-12 * 1.0 * nt, a
