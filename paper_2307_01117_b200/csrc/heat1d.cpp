@@ -310,21 +310,25 @@ int run_passes(heat1d_t h, int64_t nt) {
             int rc = launch_pass_slab(h, s, Tp, 0, s.count, wrapT);
             if (rc) return rc;
         } else {
+            // comm stream: halo exchange, then the two edge strips (K3, 2 small CTAs) as soon as
+            // the ghosts land -- concurrently with the interior pass on the compute stream, so
+            // only the exchange latency, never K3, can reach the critical path.  K2 writes
+            // B[T, n-T), K3 writes B[0,T) and B[n-T, n): disjoint; both read A.
             CK(cudaEventRecord(h->ev_ready, h->stream));
             CK(cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
             int rc = exchange(h, Tp);
             if (rc) return rc;
+            for (const Slab &s : h->slabs) {
+                CK(heat1d::launch_edges(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp, h->q,
+                                        heat1d::scale_of(h->r, Tp), h->comm));
+                h->launches++;
+            }
             CK(cudaEventRecord(h->ev_halo, h->comm));
             for (const Slab &s : h->slabs) {
                 rc = launch_pass_slab(h, s, Tp, Tp, s.count - Tp, 0);
                 if (rc) return rc;
             }
             CK(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
-            for (const Slab &s : h->slabs) {
-                CK(heat1d::launch_edges(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp, h->q,
-                                        heat1d::scale_of(h->r, Tp), h->stream));
-                h->launches++;
-            }
         }
         h->cur ^= 1;
         done += Tp;
@@ -544,7 +548,10 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     h->rank = o.rank;
     h->nranks = o.nranks;
     h->blocking = o.blocking != 0;
-    h->use_graphs = o.use_graphs != 0;
+    // Multi-rank runs do not capture NCCL calls into CUDA graphs: NCCL sets up its p2p
+    // connections lazily (cudaMalloc/IPC, illegal under capture), and a pass there is long
+    // (C4 at G=8: ~1.3 ms) next to its ~3 launches.
+    h->use_graphs = o.use_graphs != 0 && o.nranks == 1;
     h->ops = (o.mode == HEAT1D_MODE_FAST || is_pow2(r) || r == 0.0) ? 3 : 4;
     // r == 0: fma(0, t, b) == b + 0*t == b for finite t (identity either way)
     // Fast mode works on the scaled state v = u / r^t (stencil.cuh, DESIGN.md §3 c21): 1 DP op per
@@ -677,6 +684,15 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
             h->nccl = nullptr;
             set_error(nullptr, HEAT1D_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(ne));
             return bail(HEAT1D_ENCCL);
+        }
+        // one warm-up exchange (contents irrelevant: the first pass's exchange overwrites the
+        // pads) so NCCL's p2p connections exist before the first timed pass and a broken
+        // transport fails here, at create
+        int rc = exchange(h, h->T);
+        if (rc == HEAT1D_OK && cudaStreamSynchronize(h->comm) != cudaSuccess) rc = HEAT1D_ECUDA;
+        if (rc) {
+            set_error(nullptr, rc, "warm-up halo exchange failed: %s", h->last_error.c_str());
+            return bail(rc);
         }
     }
     if (!parse_geom_env(&h->geom)) h->geom = heat1d::choose_geom(h->slabs[0].count, h->T, h->num_sms);
