@@ -310,9 +310,7 @@ def measure(h1, cfg, mode, args, world, rank, local_rank, stream, u0_dev, with_e
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            h.set_initial(host_in)
-            h.run(cfg.nt)
-            h.get(host_out)
+            h.solve_host(host_in, cfg.nt, host_out)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -323,7 +321,8 @@ def measure(h1, cfg, mode, args, world, rank, local_rank, stream, u0_dev, with_e
             ems = float(t.item())
         e2e = {"value": updates / (ems / 1e3) / 1e9, "unit": "GLUPS", "h2d_bytes_per_step": 8 * count,
                "d2h_bytes_per_step": 8 * count, "ms_per_step": ems / args.steps,
-               "path": "heat1d_set_initial(pinned host) + heat1d_run + heat1d_get(pinned host)"}
+               "path": "heat1d_solve_host(pinned host u0 -> nt steps -> pinned host out)",
+               "windows": h.info()["stream_windows"]}
         del host_in, host_out
     roof = kernel_roofline(info, cfg, count, world, args.steps, k2_launches, k2_ms, ms, value, mode)
     h.close()

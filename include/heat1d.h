@@ -117,6 +117,7 @@ typedef struct {
     int32_t pass_V, pass_NW, pass_S; /* cells/lane, compute warps/CTA, TMA stages            */
     int32_t resident;       /* 1 if runs use the register-resident kernel K6                */
     int32_t resident_warps; /* warps of the last K6 launch                                  */
+    int64_t stream_windows; /* light-cone windows of the last heat1d_solve_host (0: plain)  */
 } heat1d_info_t;
 
 /* Exchange plan of one rank (pure host logic; usable without a GPU).  Offsets
@@ -180,6 +181,22 @@ HEAT1D_API int heat1d_run(heat1d_t h, int64_t nt);
 
 /* Copy this slab's current state to out (host or device pointer), synchronous. */
 HEAT1D_API int heat1d_get(heat1d_t h, double *out, int64_t count);
+
+/* One whole solve between HOST arrays with the transfers hidden behind the compute:
+ * u0 (count = local n cells) -> nt steps -> out (count cells); same result as
+ * heat1d_set_initial(u0) + heat1d_run(nt) + heat1d_get(out) (bitwise in matched mode).
+ * By the domain of dependence of Eq. 2 (a cell at step t depends on
+ * cells within t of it at step 0), the ring is cut into C chunks and each chunk is
+ * solved on its own light-cone window [chunk - nt, chunk + nt) (indices mod N); the
+ * H2D copy of window c+1 and the D2H copy of chunk c-1 run on their own streams while
+ * window c computes, so a solve costs ~max(transfers, compute) instead of their sum.
+ * Used for one slab on one rank when the chunks are >= 16 nt cells (redundant work
+ * <= 2nt/chunk); otherwise it IS the plain three-call sequence.  u0/out should be
+ * pinned (cudaHostAlloc / torch pin_memory) for the copies to overlap.  In fast mode
+ * every window checks its own max|u0| (K5) and is recomputed with the 3-op form if
+ * the scaled state could overflow (DESIGN.md c21).  Afterwards the device state is
+ * consumed: call set_initial before run/get.  Errors as set_initial/run/get. */
+HEAT1D_API int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, double *out);
 
 HEAT1D_API int64_t heat1d_steps_done(heat1d_t h);   /* -1 if h is NULL */
 HEAT1D_API int heat1d_info(heat1d_t h, heat1d_info_t *info);

@@ -20,6 +20,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -67,6 +68,12 @@ struct heat1d_s {
 
     cudaStream_t stream = nullptr, comm = nullptr;
     bool own_stream = false, own_comm = false;
+    // heat1d_solve_host: copy streams, per-slot events, per-window max|u0| words
+    cudaStream_t st_h2d = nullptr, st_d2h = nullptr;
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+    unsigned long long *win_absmax = nullptr;
+    int64_t win_absmax_n = 0;
+    int64_t stream_windows = 0;  // windows of the last heat1d_solve_host (0 = plain sequence)
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     ncclComm_t nccl = nullptr;
     void *alloc = nullptr;
@@ -820,6 +827,157 @@ int heat1d_get(heat1d_t h, double *out, int64_t count) {
     return HEAT1D_OK;
 }
 
+// ------------------------------------------------------------------ heat1d_solve_host
+namespace {
+
+// Copy ring cells [a, a+len) (indices mod n, at most one wrap per side) host -> device.
+int copy_window_in(heat1d_t h, double *dst, const double *u0, int64_t n, int64_t a, int64_t len) {
+    int64_t done = 0;
+    while (done < len) {
+        int64_t g = (a + done) % n;
+        if (g < 0) g += n;
+        const int64_t run = std::min(len - done, n - g);
+        CK(cudaMemcpyAsync(dst + done, u0 + g, (size_t)run * 8, cudaMemcpyHostToDevice, h->st_h2d));
+        done += run;
+    }
+    return HEAT1D_OK;
+}
+
+// nt steps of one light-cone window X[0, Lw) on the compute stream (ping-pong with Y);
+// pass p writes only the cells still inside the cone.  Returns the result buffer.
+int solve_window(heat1d_t h, int ops, double *X, double *Y, int64_t Lw, int64_t nt, double **res) {
+    const double q = heat1d::ops_scaled(ops) ? (1.0 - 2.0 * h->r) / h->r : h->r;
+    double *a = X, *b = Y;
+    int64_t done = 0;
+    while (done < nt) {
+        const int Tp = (int)std::min<int64_t>(h->T, nt - done);
+        int grid = 0;
+        CK(heat1d::launch_pass(h->geom, ops, a, b, Lw, Tp, done + Tp, Lw - done - Tp, 0, q,
+                               heat1d::scale_of(h->r, Tp), h->num_sms, h->stream, &grid));
+        h->launches++;
+        std::swap(a, b);
+        done += Tp;
+    }
+    *res = a;
+    return HEAT1D_OK;
+}
+
+int ensure_stream_objects(heat1d_t h, int64_t nwin) {
+    if (!h->st_h2d) CK(cudaStreamCreateWithFlags(&h->st_h2d, cudaStreamNonBlocking));
+    if (!h->st_d2h) CK(cudaStreamCreateWithFlags(&h->st_d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+        if (!h->ev_in[i]) CK(cudaEventCreateWithFlags(&h->ev_in[i], cudaEventDisableTiming));
+        if (!h->ev_comp[i]) CK(cudaEventCreateWithFlags(&h->ev_comp[i], cudaEventDisableTiming));
+        if (!h->ev_out[i]) CK(cudaEventCreateWithFlags(&h->ev_out[i], cudaEventDisableTiming));
+    }
+    if (h->win_absmax_n < nwin) {
+        if (h->win_absmax) CK(cudaFree(h->win_absmax));
+        h->win_absmax = nullptr;
+        h->win_absmax_n = 0;
+        CK(cudaMalloc(&h->win_absmax, (size_t)nwin * sizeof(unsigned long long)));
+        h->win_absmax_n = nwin;
+    }
+    return HEAT1D_OK;
+}
+
+bool fast_range_ok(heat1d_t h, unsigned long long bits) {
+    double m;
+    memcpy(&m, &bits, sizeof m);
+    int e = 0;
+    if (std::isfinite(m)) std::frexp(m, &e);
+    return std::isfinite(m) && (double)e + (double)h->T * std::log2(1.0 / h->r) < 1000.0;
+}
+
+// Window plan: C chunks of L cells, windows of L + 2H cells (H = nt), two slots of two
+// ping-pong buffers carved out of the handle's two ring buffers.  false = not worth it.
+bool stream_plan(heat1d_t h, int64_t nt, int64_t *C, int64_t *L, int64_t *half) {
+    if (h->multi() || h->resident || h->kernel == HEAT1D_KERNEL_NAIVE || nt < 1) return false;
+    const int64_t n = h->slabs[0].count;
+    const int64_t cap = round_up(n + 2 * h->pad, 32);  // doubles per ring buffer
+    *half = cap / 2 / 32 * 32;
+    const int64_t lw_max = *half - 2 * h->pad;
+    const int64_t lmax = lw_max - 2 * nt;
+    if (lmax < 16 * nt || lmax < 4096) return false;
+    // up to 16 windows when the ring allows (pipeline fill + drain ~ 2/C of the transfers)
+    int64_t c = (n + lmax - 1) / lmax;
+    while (c < 16 && (n / (c + 1)) >= 16 * nt && n / (c + 1) >= (int64_t)1 << 22) ++c;
+    *C = c;
+    *L = (n + c - 1) / c;
+    return *L + 2 * nt <= lw_max;
+}
+
+}  // namespace
+
+int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, double *out) {
+    int rc = guard(h);
+    if (rc) return rc;
+    if (!u0 || !out) return set_error(h, HEAT1D_EINVAL, "u0/out is NULL");
+    if (count != h->count)
+        return set_error(h, HEAT1D_EINVAL, "count %lld != local slab %lld", (long long)count, (long long)h->count);
+    if (nt < 0) nt = h->nt_default;
+    int64_t C = 0, L = 0, half = 0;
+    if (!stream_plan(h, nt, &C, &L, &half)) {  // the plain sequence
+        rc = heat1d_set_initial(h, u0, count);
+        if (!rc) rc = heat1d_run(h, nt);
+        if (!rc) rc = heat1d_get(h, out, count);
+        return rc;
+    }
+    rc = ensure_stream_objects(h, C);
+    if (rc) return rc;
+    const Slab &s = h->slabs[0];
+    const int64_t n = s.count;
+    const int ops = h->ops_fast ? h->ops_fast : h->ops;  // optimistic; checked per window below
+    double *X[2] = {s.buf[0] + h->pad, s.buf[0] + half + h->pad};
+    double *Y[2] = {s.buf[1] + h->pad, s.buf[1] + half + h->pad};
+    h->initialized = false;  // the ring buffers now hold windows
+    if (h->ops_fast) CK(cudaMemsetAsync(h->win_absmax, 0, (size_t)C * 8, h->stream));
+    CK(cudaEventRecord(h->ev_comp[0], h->stream));  // memset before any K5
+    CK(cudaStreamWaitEvent(h->st_h2d, h->ev_comp[0], 0));
+    for (int64_t c = 0; c < C; ++c) {
+        const int sl = (int)(c & 1);
+        const int64_t a = c * L, len = std::min(L, n - a), Lw = len + 2 * nt;
+        if (c >= 2) CK(cudaStreamWaitEvent(h->st_h2d, h->ev_out[sl], 0));  // slot free again
+        rc = copy_window_in(h, X[sl], u0, n, a - nt, Lw);
+        if (rc) return rc;
+        CK(cudaEventRecord(h->ev_in[sl], h->st_h2d));
+        CK(cudaStreamWaitEvent(h->stream, h->ev_in[sl], 0));
+        if (h->ops_fast) {
+            CK(heat1d::launch_absmax(X[sl], Lw, h->win_absmax + c, h->stream));
+            h->launches++;
+        }
+        double *res = nullptr;
+        rc = solve_window(h, ops, X[sl], Y[sl], Lw, nt, &res);
+        if (rc) return rc;
+        CK(cudaEventRecord(h->ev_comp[sl], h->stream));
+        CK(cudaStreamWaitEvent(h->st_d2h, h->ev_comp[sl], 0));
+        CK(cudaMemcpyAsync(out + a, res + nt, (size_t)len * 8, cudaMemcpyDeviceToHost, h->st_d2h));
+        CK(cudaEventRecord(h->ev_out[sl], h->st_d2h));
+    }
+    CK(cudaStreamSynchronize(h->st_h2d));
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaStreamSynchronize(h->st_d2h));
+    if (h->ops_fast) {  // rare: a window whose scaled state could overflow -> redo with 3 ops
+        std::vector<unsigned long long> bits((size_t)C);
+        CK(cudaMemcpy(bits.data(), h->win_absmax, (size_t)C * 8, cudaMemcpyDeviceToHost));
+        for (int64_t c = 0; c < C; ++c) {
+            if (fast_range_ok(h, bits[(size_t)c])) continue;
+            const int64_t a = c * L, len = std::min(L, n - a), Lw = len + 2 * nt;
+            rc = copy_window_in(h, X[0], u0, n, a - nt, Lw);
+            if (rc) return rc;
+            CK(cudaEventRecord(h->ev_in[0], h->st_h2d));
+            CK(cudaStreamWaitEvent(h->stream, h->ev_in[0], 0));
+            double *res = nullptr;
+            rc = solve_window(h, 3, X[0], Y[0], Lw, nt, &res);
+            if (rc) return rc;
+            CK(cudaMemcpyAsync(out + a, res + nt, (size_t)len * 8, cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+        }
+    }
+    h->steps_done = nt;
+    h->stream_windows = C;
+    return HEAT1D_OK;
+}
+
 int64_t heat1d_steps_done(heat1d_t h) { return h ? h->steps_done : -1; }
 
 int heat1d_info(heat1d_t h, heat1d_info_t *info) {
@@ -849,6 +1007,7 @@ int heat1d_info(heat1d_t h, heat1d_info_t *info) {
     info->pass_S = h->geom.S;
     info->resident = h->resident ? 1 : 0;
     info->resident_warps = h->res_warps;
+    info->stream_windows = h->stream_windows;
     return HEAT1D_OK;
 }
 
@@ -890,6 +1049,14 @@ int heat1d_destroy(heat1d_t h) {
     if (h->alloc) cudaFree(h->alloc);
     if (h->res_scratch) cudaFree(h->res_scratch);
     if (h->absmax) cudaFree(h->absmax);
+    if (h->win_absmax) cudaFree(h->win_absmax);
+    for (int i = 0; i < 2; ++i) {
+        if (h->ev_in[i]) cudaEventDestroy(h->ev_in[i]);
+        if (h->ev_comp[i]) cudaEventDestroy(h->ev_comp[i]);
+        if (h->ev_out[i]) cudaEventDestroy(h->ev_out[i]);
+    }
+    if (h->st_h2d) cudaStreamDestroy(h->st_h2d);
+    if (h->st_d2h) cudaStreamDestroy(h->st_d2h);
     delete h;
     return HEAT1D_OK;
 }

@@ -83,6 +83,7 @@ class Info(ctypes.Structure):
         ("pass_S", ctypes.c_int32),
         ("resident", ctypes.c_int32),
         ("resident_warps", ctypes.c_int32),
+        ("stream_windows", ctypes.c_int64),
     ]
 
 
@@ -104,7 +105,7 @@ EXPORTS = (
     "heat1d_plan_exchange", "heat1d_buffer_len", "heat1d_get_unique_id", "heat1d_create",
     "heat1d_local_range", "heat1d_set_initial", "heat1d_init_uniform", "heat1d_run",
     "heat1d_get", "heat1d_steps_done", "heat1d_info", "heat1d_set_profiling",
-    "heat1d_profile", "heat1d_stream", "heat1d_destroy", "heat1d_last_error",
+    "heat1d_profile", "heat1d_stream", "heat1d_destroy", "heat1d_last_error", "heat1d_solve_host",
 )
 
 _lib = None
@@ -140,6 +141,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "heat1d_init_uniform": (ctypes.c_int, [H, ctypes.c_uint64, ctypes.c_double, ctypes.c_double]),
         "heat1d_run": (ctypes.c_int, [H, i64]),
         "heat1d_get": (ctypes.c_int, [H, vp, i64]),
+        "heat1d_solve_host": (ctypes.c_int, [H, vp, i64, i64, vp]),
         "heat1d_steps_done": (i64, [H]),
         "heat1d_info": (ctypes.c_int, [H, ctypes.POINTER(Info)]),
         "heat1d_set_profiling": (ctypes.c_int, [H, ctypes.c_int]),
@@ -306,6 +308,19 @@ class Heat1D:
             out = np.empty(self.count, dtype=np.float64)
         ptr, n, keep = _data_ptr(out)
         _check(self._lib.heat1d_get(self._h, ctypes.c_void_p(ptr), n), self._h)
+        return out
+
+    def solve_host(self, u0, nt: Optional[int] = None, out=None):
+        """set_initial(u0) + run(nt) + get(out) for HOST arrays with the transfers
+        overlapped by light-cone windows (heat1d_solve_host); pinned tensors overlap best."""
+        if out is None:
+            out = np.empty(self.count, dtype=np.float64)
+        pi, n, keep_in = _data_ptr(u0)
+        po, m, keep_out = _data_ptr(out)
+        if n != self.count or m != self.count:
+            raise ValueError("u0 and out must hold the local slab (%d cells)" % self.count)
+        _check(self._lib.heat1d_solve_host(self._h, ctypes.c_void_p(pi), n, -1 if nt is None else nt,
+                                           ctypes.c_void_p(po)), self._h)
         return out
 
     # -- profiling of the pass kernel (CUDA events on the compute stream)

@@ -530,3 +530,56 @@ def test_c4_full_nt_windows(h1, mode):
             assert_bitwise(got, w, "C4 nt=10000 window %d" % a)
         else:
             assert np.max(np.abs(got - w)) <= 1e-12 * 1.0 * nt, a
+
+
+# ------------------------------------------------------------------ heat1d_solve_host (light-cone windows)
+@pytest.mark.parametrize("N,nt,T", [(300_001, 100, 0), (300_001, 77, 13), ((1 << 22) + 5, 300, 64)])
+def test_solve_host_windows_bitwise(h1, N, nt, T):
+    """The streamed solve (C windows of chunk + nt halo cells, transfers overlapped) equals
+    the oracle bitwise in matched mode, incl. ragged last chunk and the wrap windows."""
+    import torch
+    u0 = synth.uniform(N + nt, 0, N, -1.0, 1.0)
+    want = oracle.run(u0, 0.4, nt)
+    pin_in = torch.from_numpy(u0).pin_memory()
+    pin_out = torch.empty(N, dtype=torch.float64).pin_memory()
+    with h1.Heat1D(N, 1, nt, 0.4, 1.0, 1.0, T=T, resident=False) as h:
+        h.solve_host(pin_in, nt, pin_out)
+        assert h.info()["stream_windows"] >= 3
+        assert_bitwise(pin_out.numpy(), want, "solve_host N=%d nt=%d" % (N, nt))
+        got = h.solve_host(u0, nt)                      # pageable numpy arrays work too
+        assert_bitwise(got, want, "solve_host pageable")
+        with pytest.raises(h1.Heat1DError) as ei:      # device state consumed
+            h.run(1)
+        assert ei.value.status == 3
+        h.set_initial(u0)                               # and the handle is reusable
+        h.run(nt)
+        assert_bitwise(h.get(), want, "after solve_host")
+
+
+def test_solve_host_plain_fallback(h1):
+    """nt too large for windows, and the resident path: the plain three-call sequence."""
+    N, nt = 10_000, 2000
+    u0 = synth.uniform(12, 0, N, -1.0, 1.0)
+    want = oracle.run(u0, 0.5, nt)
+    for res in (False, None):
+        with h1.Heat1D(N, 1, nt, 0.5, 1.0, 1.0, resident=res) as h:
+            assert_bitwise(h.solve_host(u0, nt), want, "fallback res=%s" % res)
+            assert h.info()["stream_windows"] == 0
+
+
+def test_solve_host_fast_and_range_fallback(h1):
+    N, nt = 1_000_003, 150
+    u0 = synth.uniform(21, 0, N, -1.0, 1.0)
+    with h1.Heat1D(N, 1, nt, 0.25, 1.0, 1.0, mode="fast", resident=False) as h:
+        got = h.solve_host(u0, nt)
+        assert h.info()["stream_windows"] >= 3
+        assert np.max(np.abs(got - oracle.run(u0, 0.25, nt))) <= fast_bound(u0, nt)
+        big = u0 * 1e300                                # scaled state would overflow: windows redone
+        got = h.solve_host(big, nt)
+        assert np.all(np.isfinite(got))
+        assert np.max(np.abs(got - oracle.run(big, 0.25, nt))) <= fast_bound(big, nt)
+    with h1.Heat1D(N, 1, nt, 0.5, 1.0, 1.0, mode="fast", resident=False) as h:
+        want = u0.copy()
+        for _ in range(nt):
+            want = (np.roll(want, 1) + np.roll(want, -1)) * 0.5
+        assert_bitwise(h.solve_host(u0, nt), want, "r=1/2 fast windows")
