@@ -63,6 +63,11 @@ struct heat1d_s {
     PassGeom geom{49, 4, 2, 2, 4};
     int last_grid = 0;
     bool resident = false;     // K6 path
+    // K6 across ranks (or, HEAT1D_K6_MAILBOX=1, one rank routing its wrap through itself):
+    // this rank's mailbox and the neighbour ranks' (CUDA IPC peer mappings)
+    double *mbox = nullptr, *mbox_left = nullptr, *mbox_right = nullptr;
+    bool mbox_ipc_left = false, mbox_ipc_right = false;
+    unsigned k6_base = 0;  // global exchange index of the next K6 launch
     void *res_scratch = nullptr;
     int res_warps = 0;
 
@@ -277,14 +282,28 @@ int run_resident(heat1d_t h, int64_t nt) {
         if (!e0 || !e1) return set_error(h, HEAT1D_ECUDA, "event pool");
         CK(cudaEventRecord(e0, h->stream));
     }
+    heat1d::MboxArgs mb;
+    if (h->mbox) {
+        mb.self = h->mbox;
+        mb.left = h->mbox_left;
+        mb.right = h->mbox_right;
+        mb.base = h->k6_base;
+        mb.on = 1;
+        // indices base .. base+P-1 used (initial exchange + P-1 periods); skipping one more at
+        // the run boundary keeps a slot from being rewritten while a slower neighbour may
+        // still read it (resident.cu, mbox_publish)
+        h->k6_base += (unsigned)((nt + h->T - 1) / h->T) + 2u;
+    }
     CK(heat1d::launch_resident(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, h->T, nt, h->q,
-                               h->r, h->res_scratch, h->num_sms, h->stream, &h->res_warps));
+                               h->r, h->res_scratch, h->num_sms, h->stream, &h->res_warps, mb));
     h->launches++;
     if (h->prof) CK(cudaEventRecord(e1, h->stream));
     h->cur ^= 1;
-    // keep the periodic pads of the new state valid (cheap; lets any path continue)
-    CK(heat1d::launch_wrap_fill(cell0(h, s, h->cur), s.count, h->pad, h->stream));
-    h->launches++;
+    if (h->nranks == 1) {
+        // keep the periodic pads of the new state valid (cheap; lets any path continue)
+        CK(heat1d::launch_wrap_fill(cell0(h, s, h->cur), s.count, h->pad, h->stream));
+        h->launches++;
+    }
     h->steps_done += nt;
     return HEAT1D_OK;
 }
@@ -397,6 +416,60 @@ int run_maybe_graph(heat1d_t h, int64_t nt) {
     h->steps_done = s0;
     h->use_graphs = false;
     return run_passes(h, nt);
+}
+
+// K6 across ranks: agree (NCCL min-reduce) that every rank's slab fits; then allocate this
+// rank's mailbox and map the two neighbours' mailboxes (CUDA IPC handles all-gathered
+// over NCCL, opened with lazy peer access: remote stores travel over NVLink).
+int setup_multi_resident(heat1d_t h, bool local_fits) {
+    const int G = h->nranks;
+    int *dv = nullptr;
+    CK(cudaMalloc(&dv, sizeof(int)));
+    const int mine = local_fits ? 1 : 0;
+    CK(cudaMemcpy(dv, &mine, sizeof(int), cudaMemcpyHostToDevice));
+    NK(ncclAllReduce(dv, dv, 1, ncclInt32, ncclMin, h->nccl, h->comm));
+    int all = 0;
+    CK(cudaMemcpyAsync(&all, dv, sizeof(int), cudaMemcpyDeviceToHost, h->comm));
+    CK(cudaStreamSynchronize(h->comm));
+    if (!all) {
+        CK(cudaFree(dv));
+        return HEAT1D_OK;  // K2 passes + NCCL exchange
+    }
+    CK(cudaMalloc(&h->mbox, heat1d::MBOX_BYTES));
+    CK(cudaMemset(h->mbox, 0, heat1d::MBOX_BYTES));
+    cudaIpcMemHandle_t mineh;
+    CK(cudaIpcGetMemHandle(&mineh, h->mbox));
+    char *dh = nullptr;
+    CK(cudaMalloc(&dh, (size_t)G * sizeof(cudaIpcMemHandle_t)));
+    CK(cudaMemcpy(dh + (size_t)h->rank * sizeof(mineh), &mineh, sizeof(mineh), cudaMemcpyHostToDevice));
+    NK(ncclAllGather(dh + (size_t)h->rank * sizeof(mineh), dh, sizeof(mineh), ncclChar, h->nccl, h->comm));
+    std::vector<cudaIpcMemHandle_t> all_h((size_t)G);
+    CK(cudaMemcpyAsync(all_h.data(), dh, (size_t)G * sizeof(mineh), cudaMemcpyDeviceToHost, h->comm));
+    CK(cudaStreamSynchronize(h->comm));
+    CK(cudaFree(dh));
+    const int left = (h->rank - 1 + G) % G, right = (h->rank + 1) % G;
+    void *pl = nullptr, *pr = nullptr;
+    CK(cudaIpcOpenMemHandle(&pl, all_h[(size_t)left], cudaIpcMemLazyEnablePeerAccess));
+    h->mbox_left = static_cast<double *>(pl);
+    h->mbox_ipc_left = true;
+    if (right == left) {
+        pr = pl;
+    } else {
+        CK(cudaIpcOpenMemHandle(&pr, all_h[(size_t)right], cudaIpcMemLazyEnablePeerAccess));
+        h->mbox_ipc_right = true;
+    }
+    h->mbox_right = static_cast<double *>(pr);
+    // barrier: every rank's mailbox is zeroed and mapped before any rank's first K6 launch
+    CK(cudaDeviceSynchronize());
+    NK(ncclAllReduce(dv, dv, 1, ncclInt32, ncclMin, h->nccl, h->comm));
+    CK(cudaStreamSynchronize(h->comm));
+    CK(cudaFree(dv));
+    h->resident = true;
+    if (cudaMalloc(&h->res_scratch, heat1d::resident_scratch_bytes(h->T, h->num_sms)) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(h, HEAT1D_ENOMEM, "resident scratch");
+    }
+    return HEAT1D_OK;
 }
 
 int guard(heat1d_t h) {
@@ -600,20 +673,27 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     int T = o.T > 0 ? o.T : auto_T(h->ops_fast ? h->ops_fast : h->ops);
     if (o.kernel == HEAT1D_KERNEL_NAIVE) T = 1;
     if (T > mslab) T = (int)mslab;  // a slab must hold its own halo
-    const bool res_ok = (G == 1 && o.kernel == HEAT1D_KERNEL_AUTO && o.resident != 0);
+    // K6 across ranks (one slab per rank): every rank must agree, decided after NCCL init
+    bool res_multi_local = false;
+    const bool res_ok = ((G == 1) || (o.nranks > 1 && o.virtual_slabs == 1)) && o.kernel == HEAT1D_KERNEL_AUTO &&
+                        o.resident != 0;
     if (res_ok) {
-        const int64_t n0 = h->N;
+        int64_t f0 = 0, n0 = h->N;
+        if (G > 1) partition(nx, np, G, o.rank, &f0, &n0);
         // K6 period (halo refresh) <= 64; auto = 64 (V = 33 spans): half the exchanges of T = 32
         // for +32 % (C5) / +30 % (C2) measured (profiles/r01_k6_period_sync.jsonl)
         int Tr = (o.T > 0 && o.T < 64) ? o.T : 64;
-        if (Tr > n0) Tr = (int)n0;
+        if (Tr > mslab) Tr = (int)mslab;
         int coop = 0;
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
         const bool fits = coop && n0 <= heat1d::resident_capacity(Tr, h->num_sms) && n0 >= Tr &&
                           heat1d::resident_fits(h->ops, n0, Tr, h->num_sms) &&
                           (!h->ops_fast || heat1d::resident_fits(h->ops_fast, n0, Tr, h->num_sms));
         cudaGetLastError();
-        if (fits) {
+        if (fits && G > 1) {
+            res_multi_local = true;  // tentatively: T = Tr; agreed on below
+            T = Tr;
+        } else if (fits) {
             h->resident = true;
             T = Tr;
         } else if (o.resident == 1) {
@@ -701,6 +781,27 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
             set_error(nullptr, rc, "warm-up halo exchange failed: %s", h->last_error.c_str());
             return bail(rc);
         }
+        if (res_ok) {
+            rc = setup_multi_resident(h, res_multi_local);
+            if (rc) {
+                set_error(nullptr, rc, "multi-rank resident setup: %s", h->last_error.c_str());
+                return bail(rc);
+            }
+            if (!h->resident && o.resident == 1) {
+                set_error(nullptr, HEAT1D_EUNSUPPORTED, "a rank's slab does not fit the resident kernel");
+                return bail(HEAT1D_EUNSUPPORTED);
+            }
+        }
+    }
+    if (h->resident && h->nranks == 1 && getenv("HEAT1D_K6_MAILBOX") && atoi(getenv("HEAT1D_K6_MAILBOX")) == 1) {
+        // test knob: route the single rank's wrap through its own mailbox (the multi-rank protocol)
+        if (cudaMalloc(&h->mbox, heat1d::MBOX_BYTES) != cudaSuccess ||
+            cudaMemset(h->mbox, 0, heat1d::MBOX_BYTES) != cudaSuccess) {
+            cudaGetLastError();
+            set_error(nullptr, HEAT1D_ENOMEM, "mailbox");
+            return bail(HEAT1D_ENOMEM);
+        }
+        h->mbox_left = h->mbox_right = h->mbox;
     }
     if (!parse_geom_env(&h->geom)) h->geom = heat1d::choose_geom(h->slabs[0].count, h->T, h->num_sms);
     if (h->ops_fast && cudaMalloc(&h->absmax, sizeof(unsigned long long)) != cudaSuccess) {
@@ -708,7 +809,7 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
         set_error(nullptr, HEAT1D_ENOMEM, "absmax word");
         return bail(HEAT1D_ENOMEM);
     }
-    if (h->resident) {
+    if (h->resident && !h->res_scratch) {
         if (cudaMalloc(&h->res_scratch, heat1d::resident_scratch_bytes(h->T, h->num_sms)) != cudaSuccess) {
             cudaGetLastError();
             set_error(nullptr, HEAT1D_ENOMEM, "resident scratch");
@@ -1049,6 +1150,9 @@ int heat1d_destroy(heat1d_t h) {
     if (h->alloc) cudaFree(h->alloc);
     if (h->res_scratch) cudaFree(h->res_scratch);
     if (h->absmax) cudaFree(h->absmax);
+    if (h->mbox_ipc_left) cudaIpcCloseMemHandle(h->mbox_left);
+    if (h->mbox_ipc_right) cudaIpcCloseMemHandle(h->mbox_right);
+    if (h->mbox) cudaFree(h->mbox);
     if (h->win_absmax) cudaFree(h->win_absmax);
     for (int i = 0; i < 2; ++i) {
         if (h->ev_in[i]) cudaEventDestroy(h->ev_in[i]);

@@ -75,11 +75,25 @@ cudaError_t launch_absmax(const double *u, int64_t count, unsigned long long *ou
 cudaError_t launch_init_uniform(double *u, int64_t count, int64_t first, uint64_t seed,
                                 double lo, double hi, cudaStream_t st);
 
+// K6 across ranks: each rank's mailbox = double[2 sides][2 slots][MBOX_TMAX] + two flag
+// words on their own 128-byte lines at MBOX_FLAG_OFF (side 0: from the left rank, side 1:
+// from the right rank).  left/right point at the neighbour ranks' mailboxes (CUDA IPC peer
+// mappings over NVLink; == self for one rank, which routes the ring's wrap through them).
+constexpr int MBOX_TMAX = 64;
+constexpr size_t MBOX_FLAG_OFF = 2 * 2 * MBOX_TMAX * sizeof(double);
+constexpr size_t MBOX_BYTES = MBOX_FLAG_OFF + 256;
+struct MboxArgs {
+    double *self = nullptr, *left = nullptr, *right = nullptr;
+    unsigned base = 0;  // first global exchange index of this launch
+    int on = 0;
+};
+
 // K6: whole nt-step solve of a single-slab ring held in registers (resident.cu).
 int64_t resident_capacity(int T, int num_sms);
 bool resident_fits(int ops, int64_t n, int T, int num_sms);  // plan + co-residency check
 size_t resident_scratch_bytes(int T, int num_sms);
 cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
-                            double r, void *scratch, int num_sms, cudaStream_t st, int *warps_out);
+                            double r, void *scratch, int num_sms, cudaStream_t st, int *warps_out,
+                            const MboxArgs &mb = MboxArgs{});
 
 }  // namespace heat1d

@@ -43,6 +43,23 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
     return v;
 }
 
+// system scope: flags written by a peer GPU over NVLink (K6 across ranks)
+__device__ __forceinline__ void st_release_sys(unsigned *p, unsigned v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 template <int V, int OPS, bool EARLY>
 __device__ __forceinline__ void step_regs(const double (&u)[V], double (&v)[V], double &L, double &R,
                                           double r) {
@@ -151,9 +168,61 @@ __device__ __forceinline__ void publish(const Span &s, int T, unsigned p, double
     if (lane == 0) st_release(flags + s.id, p + 1);
 }
 
-// wait for the neighbours' period-p edges and write them into the halos
+// The slab's boundary spans trade halos with the neighbour RANKS through mailboxes
+// (MboxArgs, kernels.h): span 0 writes its first T owned cells into the left rank's
+// mailbox side 1, the last span its last T owned cells into the right rank's side 0,
+// with remote (NVLink) stores and a system-scope release of the slot's flag; each rank
+// reads its own mailbox.  Slots alternate with the global exchange index g (see
+// launch_resident: indices never repeat across runs, and skip one at run boundaries).
+__device__ __forceinline__ double *mbox_data(double *mb, int side, unsigned g) {
+    return mb + ((size_t)side * 2 + (g & 1)) * MBOX_TMAX;
+}
+__device__ __forceinline__ unsigned *mbox_flag(double *mb, int side) {
+    return reinterpret_cast<unsigned *>(reinterpret_cast<char *>(mb) + MBOX_FLAG_OFF) + side * 32;
+}
+
+__device__ __forceinline__ void mbox_publish(const Span &s, int Ns, int T, unsigned g, const MboxArgs &mb, int lane) {
+    if (s.id == 0) {
+        double *D = mbox_data(mb.left, 1, g);
+        for (int i = lane; i < T; i += 32) D[i] = s.row[T + i];
+        __syncwarp();
+        if (lane == 0) st_release_sys(mbox_flag(mb.left, 1), g + 1);
+    }
+    if (s.id == Ns - 1) {
+        double *D = mbox_data(mb.right, 0, g);
+        for (int i = lane; i < T; i += 32) D[i] = s.row[s.own + i];
+        __syncwarp();
+        if (lane == 0) st_release_sys(mbox_flag(mb.right, 0), g + 1);
+    }
+}
+
+// wait for the neighbours' period-p edges and write them into the halos; with mailboxes
+// on, the slab's outer halos come from the neighbour ranks (exchange index g)
+// initial: the exchange of the initial state (only the remote sides; the local halos
+// were loaded from the slab).
 __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, const double *edges,
-                                        const unsigned *flags, int lane, int sync) {
+                                        const unsigned *flags, int lane, int sync, int Ns, const MboxArgs &mb,
+                                        unsigned g, bool initial = false) {
+    const bool lrem = mb.on && s.id == 0, rrem = mb.on && s.id == Ns - 1;
+    if (lrem || rrem) {
+        const bool doL = lrem || !initial, doR = rrem || !initial;
+        const unsigned *Lf = lrem ? mbox_flag(mb.self, 0) : flags + s.left;
+        const unsigned *Rf = rrem ? mbox_flag(mb.self, 1) : flags + s.right;
+        const unsigned Lt = !doL ? 0u : lrem ? g + 1 : p + 1, Rt = !doR ? 0u : rrem ? g + 1 : p + 1;
+        while (!__all_sync(0xffffffffu, ld_relaxed_sys(Lf) >= Lt && ld_relaxed_sys(Rf) >= Rt)) {
+        }
+        if (doL) (void)ld_acquire_sys(Lf);
+        if (doR) (void)ld_acquire_sys(Rf);
+        __syncwarp();
+        const double *LE = lrem ? mbox_data(mb.self, 0, g) : edges + ((size_t)s.left * 4 + (p & 1) * 2) * T + T;
+        const double *RE = rrem ? mbox_data(mb.self, 1, g) : edges + ((size_t)s.right * 4 + (p & 1) * 2) * T;
+        for (int i = lane; i < T; i += 32) {
+            if (doL) s.row[i] = __ldcg(LE + i);
+            if (doR) s.row[s.own + T + i] = __ldcg(RE + i);
+        }
+        __syncwarp();
+        return;
+    }
     // every lane polls (one coalesced request per poll); the vote makes the exit
     // warp-uniform, so ptxas keeps the step loop's shuffles non-collective.
     // Relaxed polls: an acquire at gpu scope invalidates L1 (CCTL.IVALL) each
@@ -188,7 +257,7 @@ __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, const 
 template <int V, int OPS, int SPW, bool EARLY>
 __global__ void __launch_bounds__(256)
 k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t nt, double r,
-            double rr, double *__restrict__ edges, unsigned *__restrict__ flags, int Wt, int sync) {
+            double rr, double *__restrict__ edges, unsigned *__restrict__ flags, int Wt, int sync, MboxArgs mb) {
     extern __shared__ __align__(16) double srow[];
     const int lane = threadIdx.x & 31;
     const int wib = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);  // warp-uniform for the compiler
@@ -204,6 +273,11 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
     row_to_regs<V>(a.row, ua, lane);
 
     if constexpr (SPW == 1) {
+        if (mb.on && (a.id == 0 || a.id == Ns - 1)) {  // outer halos of the initial state: neighbour ranks
+            mbox_publish(a, Ns, T, mb.base, mb, lane);
+            refresh(a, T, 0, edges, flags, lane, sync, Ns, mb, mb.base, true);
+            row_to_regs<V>(a.row, ua, lane);
+        }
         int64_t done = 0;
         for (unsigned p = 0;; ++p) {
             const int Tp = (int)((nt - done) < T ? (nt - done) : T);
@@ -213,7 +287,8 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
             done += Tp;
             if (done >= nt) break;
             publish(a, T, p, edges, flags, lane);
-            refresh(a, T, p, edges, flags, lane, sync);
+            if (mb.on) mbox_publish(a, Ns, T, mb.base + 1 + p, mb, lane);
+            refresh(a, T, p, edges, flags, lane, sync, Ns, mb, mb.base + 1 + p);
             row_to_regs<V>(a.row, ua, lane);
         }
 #pragma unroll
@@ -235,7 +310,7 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
             regs_to_row<V>(ua, a.row, lane);
             if (!last) publish(a, T, p, edges, flags, lane);
             if (p > 0) {  // B's halos for period p: neighbours' period p-1 edges
-                refresh(b, T, p - 1, edges, flags, lane, sync);
+                refresh(b, T, p - 1, edges, flags, lane, sync, Ns, MboxArgs{}, 0u);
                 row_to_regs<V>(b.row, ub, lane);
             }
             steps_regs<V, OPS, EARLY>(ub, v, Tp, r, sc);
@@ -243,7 +318,7 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
             if (!last) publish(b, T, p, edges, flags, lane);
             done += Tp;
             if (last) break;
-            refresh(a, T, p, edges, flags, lane, sync);  // overlapped with B's compute above
+            refresh(a, T, p, edges, flags, lane, sync, Ns, MboxArgs{}, 0u);  // overlapped with B's compute above
             row_to_regs<V>(a.row, ua, lane);
         }
 #pragma unroll
@@ -308,7 +383,7 @@ cudaError_t res_attr(const void *fn) {
 
 // Split the ring into Ns = spw*Wt equal spans (each owning >= T cells, span
 // own + 2T <= 32*RV) with warps balanced across SMs.
-bool res_plan(int ops, int64_t n, int T, int num_sms, ResPlan *p) {
+bool res_plan(int ops, int64_t n, int T, int num_sms, ResPlan *p, bool mbox = false) {
     const int RV = rv_of(T);
     p->rv = RV;
     const int cap = 32 * RV - 2 * T;
@@ -316,7 +391,8 @@ bool res_plan(int ops, int64_t n, int T, int num_sms, ResPlan *p) {
     // 1 span per warp by default (profiles/r01_k6_ab_*.jsonl: 2 spans per warp do
     // not pay on B200); HEAT1D_K6_SPW=2 selects the alternating two-span warps.
     p->spw = 1;
-    if (const char *e = getenv("HEAT1D_K6_SPW")) p->spw = (atoi(e) == 2 && n >= 2 * (int64_t)T && RV == 17) ? 2 : 1;
+    if (const char *e = getenv("HEAT1D_K6_SPW"))
+        p->spw = (atoi(e) == 2 && n >= 2 * (int64_t)T && RV == 17 && !mbox) ? 2 : 1;
     const int64_t ns_min = (n + cap - 1) / cap;
     const int64_t wt_min = (ns_min + p->spw - 1) / p->spw;
     if (wt_min <= num_sms) {
@@ -357,7 +433,7 @@ int64_t resident_capacity(int T, int num_sms) {
 
 bool resident_fits(int ops, int64_t n, int T, int num_sms) {
     ResPlan p;
-    return res_plan(ops, n, T, num_sms, &p);
+    return res_plan(ops, n, T, num_sms, &p, false);
 }
 
 size_t resident_scratch_bytes(int T, int num_sms) {
@@ -366,9 +442,10 @@ size_t resident_scratch_bytes(int T, int num_sms) {
 }
 
 cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
-                            double r, void *scratch, int num_sms, cudaStream_t st, int *warps_out) {
+                            double r, void *scratch, int num_sms, cudaStream_t st, int *warps_out,
+                            const MboxArgs &mb) {
     ResPlan p;
-    if (!res_plan(ops, n, T, num_sms, &p)) return cudaErrorInvalidValue;
+    if (!res_plan(ops, n, T, num_sms, &p, mb.on != 0)) return cudaErrorInvalidValue;
     const int64_t ns = p.wt * p.spw;
     double *edges = static_cast<double *>(scratch);
     unsigned *flags = reinterpret_cast<unsigned *>(edges + (size_t)ns * 4 * T);
@@ -377,7 +454,7 @@ cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int 
     int Wt = (int)p.wt;
     int sync = res_sync();
     void *args[] = {(void *)&A, (void *)&B, (void *)&n, (void *)&T, (void *)&nt, (void *)&q, (void *)&r,
-                    (void *)&edges, (void *)&flags, (void *)&Wt, (void *)&sync};
+                    (void *)&edges, (void *)&flags, (void *)&Wt, (void *)&sync, (void *)&mb};
     if (warps_out) *warps_out = Wt;
     if (getenv("HEAT1D_DEBUG"))
         fprintf(stderr, "[heat1d] K6 n=%lld T=%d spw=%d Wt=%d nw=%lld grid=%lld smem=%zu\n", (long long)n, T,

@@ -131,6 +131,29 @@ def test_resident_sync_variants(h1, monkeypatch, sync):
             assert_bitwise(h.get(), oracle.run(u0, 0.4, nt), "K6 sync=%s N=%d" % (sync, N))
 
 
+@pytest.mark.parametrize("N,T", [(40, 8), (545, 16), (100_003, 32), (1 << 20, 64), (1_000_000, 64)])
+def test_resident_mailbox_loopback(h1, monkeypatch, N, T):
+    """K6 with the multi-rank mailbox protocol (remote-store halos + system-scope flags,
+    initial-state exchange, global exchange indices across runs) on one rank whose ring
+    wrap is routed through its own mailbox (HEAT1D_K6_MAILBOX=1): bitwise = oracle over
+    several consecutive runs, incl. tail periods; fast mode within the bound."""
+    monkeypatch.setenv("HEAT1D_K6_MAILBOX", "1")
+    u0 = synth.uniform(N + T, 0, N, -1.0, 1.0)
+    with h1.Heat1D(N, 1, 0, 0.4, 1.0, 1.0, T=T, resident=True) as h:
+        assert h.info()["resident"] == 1
+        h.set_initial(u0)
+        want = u0
+        for nt in (3 * T + 2, T, 1, 2 * T):
+            h.run(nt)
+            want = oracle.run(want, 0.4, nt)
+            assert_bitwise(h.get(), want, "mailbox N=%d T=%d after +%d" % (N, T, nt))
+    nt = 2 * T + 3
+    with h1.Heat1D(N, 1, nt, 0.5, 1.0, 1.0, T=T, resident=True, mode="fast") as h:
+        h.set_initial(u0)
+        h.run()
+        assert np.max(np.abs(h.get() - oracle.run(u0, 0.5, nt))) <= fast_bound(u0, nt)
+
+
 def test_resident_refuses_too_large(h1):
     with pytest.raises(h1.Heat1DError) as ei:
         h1.Heat1D(1 << 24, 1, 10, 0.5, 1.0, 1.0, resident=True)
