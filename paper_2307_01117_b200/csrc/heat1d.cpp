@@ -182,13 +182,12 @@ int64_t min_slab(int64_t nx, int64_t np, int32_t G) {
 }
 
 int auto_T(int ops) {
-    // DESIGN.md §6 (T sweeps in profiles/r01_sweep_*.jsonl): each pass moves
-    // 16/T bytes per update, so T is raised until the pass is fp64-issue bound;
-    // with the inter-warp ghost exchange (kind 4) the extra work of a deeper
-    // pass is only the CTA-edge trapezoid 2T/(NW 32V), so T = 64 is at or
-    // within 1 % of the best measured T for all four arithmetic variants.
-    (void)ops;
-    return 64;
+    // DESIGN.md §6 (T sweeps in profiles/r01_sweep_kx.jsonl, r01_c3_tsweep.md): each pass
+    // moves 16/T bytes per update, so T is raised until the pass is fp64-issue bound; with
+    // the inter-warp ghost exchange (kind 4) the extra work of a deeper pass is only the
+    // CTA-edge trapezoid 2T/(NW 32V).  T = 64 is within 1 % of the best measured T for the
+    // 2-, 3- and 4-op forms; the 1-op form (fast, r = 1/2) gains another 1.8 % at T = 96.
+    return ops == 1 ? 96 : 64;
 }
 
 bool parse_geom_env(PassGeom *g) {

@@ -574,7 +574,7 @@ PassFn pass_fn(int kind) {
 }
 
 // kinds 3 and 4 (inter-warp ghost exchange) for all four arithmetic variants
-#define HEAT1D_GEOMS_X(X) X(17, 4, 3) X(17, 8, 3) X(25, 4, 3) X(33, 4, 3) X(33, 8, 2) X(33, 8, 3) X(41, 4, 2) X(49, 4, 2) X(49, 8, 2) X(53, 4, 2) X(65, 4, 2)
+#define HEAT1D_GEOMS_X(X) X(17, 4, 3) X(17, 8, 3) X(25, 4, 3) X(25, 8, 2) X(33, 6, 2) X(33, 4, 2) X(33, 4, 3) X(33, 8, 2) X(33, 8, 3) X(41, 4, 2) X(49, 4, 2) X(49, 8, 2) X(53, 4, 2) X(65, 4, 2)
 
 template <int V, int NW, int S, int KX>
 PassFn pass_fn_x(int ops) {

@@ -36,6 +36,7 @@ def main():
             os.environ.pop("HEAT1D_GEOM", None)
         for k in a.k:
             for T in a.T:
+              try:
                 with h1.Heat1D(a.N, 1, a.nt, k, 1.0, 1.0, T=T, mode=a.mode, stream=st) as h:
                     h.init_uniform(1234, -1.0, 1.0)
                     h.run(a.nt)
@@ -53,6 +54,9 @@ def main():
                 print(json.dumps({"geom": g or "auto", "k": k, "T": T, "ops": info["dp_ops"], "mode": a.mode,
                                   "glups": round(glups, 1), "frac": round(glups / roof, 3), "ms": round(best, 3),
                                   "grid": info["grid"], "tile": info["tile_cells"]}), flush=True)
+              except Exception as e:  # noqa: BLE001 -- an invalid geometry for this T: skip the point
+                print(json.dumps({"geom": g or "auto", "k": k, "T": T, "mode": a.mode, "error": str(e)[:120]}),
+                      flush=True)
 
 
 if __name__ == "__main__":
