@@ -168,7 +168,9 @@ def reference_arm(args, cfg, rank):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GLUPS", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "N": cfg.N, "nx": cfg.nx, "np": cfg.np, "nt": cfg.nt, "k": cfg.k},
+        "config": {"workload": cfg.name, "N": cfg.N, "nx": cfg.nx, "np": cfg.np, "nt": cfg.nt, "k": cfg.k,
+                   "dt": cfg.dt, "dx": cfg.dx, "mode": "oracle (canonical order, bitwise = matched mode)",
+                   "parallelism": "cpu, 1 core"},
         "cpu_baseline": {"value": value, "unit": "GLUPS", "cores": host_cores_used(), "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": value, "unit": "GLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -200,7 +202,8 @@ def kernel_roofline(info, cfg, count, world, steps, k2_launches, k2_ms, ms, valu
     fp64_term = FP64_TFLOPS * 1e3 / 4.0                      # GLUPS bound by FP64 peak / 4 flop
     bj_roof = min(hbm_term, fp64_term) * world
     kind = info["pass_kind"]
-    kernel = ("k6_resident<V=17>" if info["resident"] else
+    k6v = 17 if T <= 32 else 33 if T <= 64 else 49          # resident.cu rv_of(T)
+    kernel = ("k6_resident<V=%d>" % k6v if info["resident"] else
               ["k2_pass", "k2w_pass", "k2p_pass", "k2p_pass", "k2p_pass"][kind] + "<V=%d,NW=%d,S=%d%s>" % (
                   info["pass_V"], info["pass_NW"], info["pass_S"],
                   {3: ",KX=8", 4: ",KX=16"}.get(kind, ""))) + "<OPS=%d>" % info["dp_ops"]

@@ -679,9 +679,12 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     if (res_ok) {
         int64_t f0 = 0, n0 = h->N;
         if (G > 1) partition(nx, np, G, o.rank, &f0, &n0);
-        // K6 period (halo refresh) <= 64; auto = 64 (V = 33 spans): half the exchanges of T = 32
+        // K6 period (halo refresh) <= 128; auto = 64 (V = 33 spans): half the exchanges of T = 32
         // for +32 % (C5) / +30 % (C2) measured (profiles/r01_k6_period_sync.jsonl)
-        int Tr = (o.T > 0 && o.T < 64) ? o.T : 64;
+        // (matched 3/4-op forms: T = 128 with V = 49 spans, +11 % on C5/C2; the fast forms lose
+        // occupancy to V = 49's registers and stay at 64: profiles/r01_k6_period_v49.jsonl)
+        const int ops_k6 = h->ops_fast ? h->ops_fast : h->ops;
+        int Tr = o.T > 0 ? std::min(o.T, 128) : (ops_k6 >= 3 ? 128 : 64);
         if (Tr > mslab) Tr = (int)mslab;
         int coop = 0;
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);

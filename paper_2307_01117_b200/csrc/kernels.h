@@ -79,7 +79,7 @@ cudaError_t launch_init_uniform(double *u, int64_t count, int64_t first, uint64_
 // words on their own 128-byte lines at MBOX_FLAG_OFF (side 0: from the left rank, side 1:
 // from the right rank).  left/right point at the neighbour ranks' mailboxes (CUDA IPC peer
 // mappings over NVLink; == self for one rank, which routes the ring's wrap through them).
-constexpr int MBOX_TMAX = 64;
+constexpr int MBOX_TMAX = 128;
 constexpr size_t MBOX_FLAG_OFF = 2 * 2 * MBOX_TMAX * sizeof(double);
 constexpr size_t MBOX_BYTES = MBOX_FLAG_OFF + 256;
 struct MboxArgs {

@@ -331,11 +331,11 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
 }
 
 namespace {
-// cells per lane: 17 for periods T <= 32, 33 for 32 < T <= 64 (span 32V >= own + 2T)
-int rv_of(int T) { return T > 32 ? 33 : 17; }
+// cells per lane: 17 for periods T <= 32, 33 for 32 < T <= 64, 49 up to 128 (span 32V >= own + 2T)
+int rv_of(int T) { return T > 64 ? 49 : T > 32 ? 33 : 17; }
 // warps per SM the register budget allows: V=17: ~100 regs (1 span/warp), ~156 (2 spans/warp);
 // V=33: ~128 regs (1 span/warp only)
-int max_wps(int rv, int spw) { return rv == 33 ? 15 : spw == 1 ? 20 : 12; }
+int max_wps(int rv, int spw) { return rv == 49 ? 9 : rv == 33 ? 15 : spw == 1 ? 20 : 12; }
 constexpr int MAX_WPS_ANY = 20;
 constexpr int MAX_NW = 8;     // warps per CTA (__launch_bounds__(256))
 
@@ -359,6 +359,7 @@ const void *res_fn(int ops, int spw, int rv) {
     const bool early = res_early() != 0;
 #define RF(v, o, s, e) (const void *)&k6_resident<v, o, s, e>
 #define RF_OPS(v, s, e) (ops == 4 ? RF(v, 4, s, e) : ops == 3 ? RF(v, 3, s, e) : ops == 2 ? RF(v, 2, s, e) : RF(v, 1, s, e))
+    if (rv == 49) return early ? RF_OPS(49, 1, true) : RF_OPS(49, 1, false);
     if (rv == 33) return early ? RF_OPS(33, 1, true) : RF_OPS(33, 1, false);
     if (spw == 1) return early ? RF_OPS(17, 1, true) : RF_OPS(17, 1, false);
     return early ? RF_OPS(17, 2, true) : RF_OPS(17, 2, false);

@@ -87,7 +87,7 @@ def test_ragged_multi_tile(h1, N, T, k, resident):
 
 
 @pytest.mark.parametrize("N", [1, 2, 7, 33, 544, 545, 5000, 80_000, 1_000_000, 1_400_000])
-@pytest.mark.parametrize("T", [1, 5, 16, 32, 33, 64])
+@pytest.mark.parametrize("T", [1, 5, 16, 32, 33, 64, 96, 128])
 def test_resident_kernel(h1, N, T):
     """K6 (whole solve in one cooperative launch, slab in registers) vs the oracle:
     one warp, a few warps, one warp per SM, many warps per SM, near capacity."""
@@ -131,7 +131,8 @@ def test_resident_sync_variants(h1, monkeypatch, sync):
             assert_bitwise(h.get(), oracle.run(u0, 0.4, nt), "K6 sync=%s N=%d" % (sync, N))
 
 
-@pytest.mark.parametrize("N,T", [(40, 8), (545, 16), (100_003, 32), (1 << 20, 64), (1_000_000, 64)])
+@pytest.mark.parametrize("N,T", [(40, 8), (545, 16), (100_003, 32), (1 << 20, 64), (1_000_000, 64),
+                                 (1 << 20, 128)])
 def test_resident_mailbox_loopback(h1, monkeypatch, N, T):
     """K6 with the multi-rank mailbox protocol (remote-store halos + system-scope flags,
     initial-state exchange, global exchange indices across runs) on one rank whose ring
