@@ -607,3 +607,39 @@ def test_solve_host_fast_and_range_fallback(h1):
         for _ in range(nt):
             want = (np.roll(want, 1) + np.roll(want, -1)) * 0.5
         assert_bitwise(h.solve_host(u0, nt), want, "r=1/2 fast windows")
+
+
+def test_ring_beyond_2pow32_cells(h1):
+    """Maximum-size case: a ring of 2^32 + 12345 cells (2 x 32 GiB of state) -- every cell,
+    tile and launch index is 64-bit -- checked with O3 windows around 2^31, 2^32 and the
+    wrap after 100 steps, both modes."""
+    import torch
+    N, nt, k = (1 << 32) + 12345, 100, 0.4
+    W = 256
+    starts = [0, (1 << 31) - W // 2, (1 << 32) - W // 2, N - W // 2, 3_000_000_001]
+
+    def ring_u0(first, count):  # u0 on ring cells [first, first+count) mod N, in contiguous pieces
+        parts, i = [], first % N
+        while count > 0:
+            run = min(count, N - i)
+            parts.append(synth.uniform(99, i, run, -1.0, 1.0))
+            count -= run
+            i = 0
+        return np.concatenate(parts)
+
+    want = {a: oracle.window(ring_u0(a - nt, W + 2 * nt), nt, k) for a in starts}
+    for mode in ("matched", "fast"):
+        with h1.Heat1D(N, 1, nt, k, 1.0, 1.0, mode=mode) as h:
+            h.init_uniform(99, -1.0, 1.0)
+            h.run()
+            out = torch.empty(N, dtype=torch.float64, device="cuda")
+            h.get(out)
+        for a in starts:
+            idx = (np.arange(a, a + W) % N).astype(np.int64)
+            got = out[torch.from_numpy(idx).cuda()].cpu().numpy()
+            if mode == "matched":
+                assert_bitwise(got, want[a], "2^32 ring window %d" % a)
+            else:
+                assert np.max(np.abs(got - want[a])) <= 1e-12 * nt, a
+        del out
+        torch.cuda.empty_cache()
