@@ -940,7 +940,7 @@ int copy_window_in(heat1d_t h, double *dst, const double *u0, int64_t n, int64_t
         int64_t g = (a + done) % n;
         if (g < 0) g += n;
         const int64_t run = std::min(len - done, n - g);
-        CK(cudaMemcpyAsync(dst + done, u0 + g, (size_t)run * 8, cudaMemcpyHostToDevice, h->st_h2d));
+        CK(cudaMemcpyAsync(dst + done, u0 + g, (size_t)run * 8, cudaMemcpyDefault, h->st_h2d));
         done += run;
     }
     return HEAT1D_OK;
@@ -1053,7 +1053,7 @@ int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, d
         if (rc) return rc;
         CK(cudaEventRecord(h->ev_comp[sl], h->stream));
         CK(cudaStreamWaitEvent(h->st_d2h, h->ev_comp[sl], 0));
-        CK(cudaMemcpyAsync(out + a, res + nt, (size_t)len * 8, cudaMemcpyDeviceToHost, h->st_d2h));
+        CK(cudaMemcpyAsync(out + a, res + nt, (size_t)len * 8, cudaMemcpyDefault, h->st_d2h));
         CK(cudaEventRecord(h->ev_out[sl], h->st_d2h));
     }
     CK(cudaStreamSynchronize(h->st_h2d));
@@ -1072,7 +1072,7 @@ int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, d
             double *res = nullptr;
             rc = solve_window(h, 3, X[0], Y[0], Lw, nt, &res);
             if (rc) return rc;
-            CK(cudaMemcpyAsync(out + a, res + nt, (size_t)len * 8, cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaMemcpyAsync(out + a, res + nt, (size_t)len * 8, cudaMemcpyDefault, h->stream));
             CK(cudaStreamSynchronize(h->stream));
         }
     }

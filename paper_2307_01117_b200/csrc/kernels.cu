@@ -59,6 +59,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     }
 }
 
+// Producer-side wait: the tile it waits for takes ~10 us of compute, so poll with a
+// ~0.25 us back-off sleep -- a spinning (or hardware-suspend-retrying) producer warp
+// otherwise takes ~7 % of the issue slots of the SM sub-partition it shares with
+// compute warps (ncu: NANOSLEEP.SYNCS retry loop, profiles/r01_ncu_k2p_c4_fast_T96.txt).
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) __nanosleep(256);
+}
+
 // Same, but the waiting thread is suspended in hardware until the phase completes (or the
 // time hint, in ns, runs out) instead of re-issuing try_wait: a waiting warp then takes no
 // issue slots from the compute warps sharing its SM sub-partition.
@@ -453,7 +461,7 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
             const int64_t x1 = min(x0 + W, out_hi);
             const int64_t lo = x0 - T;
             const int64_t ld_lo = lo - (lo & 1);
-            mbar_wait_sleep(&done[s], (uint32_t)((k / S) & 1));
+            mbar_wait_backoff(&done[s], (uint32_t)((k / S) & 1));
             // scalar leftovers: an odd first/last cell and the periodic self-halo
             if (lane == 0 && (x0 & 1)) B[x0] = st[x0 - ld_lo];
             if (lane == 1 && (x1 & 1) && x1 - 1 >= x0) B[x1 - 1] = st[x1 - 1 - ld_lo];
