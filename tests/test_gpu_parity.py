@@ -68,6 +68,34 @@ def test_tiny_rings(h1, N, k, T):
     assert_bitwise(gpu_run(h1, u0, N, 1, nt, k, T=T), want, "N=%d" % N)
 
 
+@pytest.mark.parametrize("N", [1, 2, 3, 5, 8, 13, 33, 100])
+@pytest.mark.parametrize("k", [0.25, 0.5, 0.4])
+def test_tiny_rings_fast_mode(h1, N, k):
+    """Fast mode on degenerate rings (N smaller than T, N = 1 and 2) through every kernel choice."""
+    u0 = synth.uniform(N + 500, 0, N, -1.0, 1.0)
+    nt = 41
+    want = oracle.run(u0, k, nt)
+    for kw in ({"T": 0}, {"T": 3, "resident": False}, {"kernel": "naive"}):
+        got = gpu_run(h1, u0, N, 1, nt, k, mode="fast", **kw)
+        assert np.max(np.abs(got - want)) <= fast_bound(u0, nt), (N, k, kw)
+
+
+def test_fast_mode_cumulative_runs_and_paper_denominator(h1):
+    """Fast mode over several run() calls (tail passes, graph replays) and with the
+    paper-literal 2h denominator (r = k dt / (2 dx) = 0.45 -> the 2-op scaled form)."""
+    N = 500_009
+    u0 = synth.uniform(77, 0, N, -1.0, 1.0)
+    with h1.Heat1D(N, 1, 0, 0.9, 1.0, 1.0, mode="fast", denominator="paper_2dx", resident=False) as h:
+        assert abs(h.info()["r"] - 0.45) < 1e-15
+        h.set_initial(u0)
+        assert h.info()["dp_ops"] == 2
+        for nt in (100, 7, 100, 64):
+            h.run(nt)
+        got = h.get()
+    r = oracle.r_of(0.9, 1.0, 1.0, paper_2h=True)
+    assert np.max(np.abs(got - oracle.run(u0, r, 271))) <= fast_bound(u0, 271)
+
+
 def test_zero_diffusivity_identity(h1):
     u0 = synth.uniform(3, 0, 5000)
     assert_bitwise(gpu_run(h1, u0, 5000, 1, 10, 0.0, T=4), u0, "k=0")
