@@ -403,6 +403,9 @@ def main():
                        "parity": ("bitwise = oracle" if args.mode == "matched"
                                   else "<= 1e-12*max|u0|*nt vs oracle (north_star fast-mode bound)"),
                        "dp_ops": info["dp_ops"], "parallelism": "slabs%d" % world,
+                       "halo_transport": ("none (one slab)" if world == 1 else
+                                          "k6 mailbox (NVLink peer memory)" if info["resident"] else
+                                          ["nccl send/recv", "p2p puts from K3 (NVLink peer memory)"][info["transport"]]),
                        "l2": "inputs larger than L2" if 16 * cfg.N // world > 126 * 2 ** 20
                        else "L2-resident ring (no flush; each step re-reads u0 from HBM copy)",
                        "tile_cells": info["tile_cells"], "grid": info["grid"]},

@@ -69,6 +69,14 @@ enum {
     HEAT1D_KERNEL_NAIVE = 1   /* one step per launch, modular indexing (K1; T forced to 1)    */
 };
 
+enum {
+    HEAT1D_TRANSPORT_NCCL = 0, /* halo exchange of several slabs: ncclSend/ncclRecv (ranks) or
+                                  device copies (virtual slabs), then the edge kernel K3      */
+    HEAT1D_TRANSPORT_P2P = 1   /* K3 itself puts its new edge strips into the neighbours' ghost
+                                  pads (NVLink peer memory via CUDA IPC for ranks) and releases
+                                  a system-scope flag the neighbour's next K3 acquires        */
+};
+
 #define HEAT1D_T_MAX 128
 
 /* Options.  Always initialise with heat1d_opts_default(); `size` versions the struct. */
@@ -96,6 +104,9 @@ typedef struct {
     void *stream;           /* cudaStream_t for compute (e.g. torch's current stream);
                                NULL = a stream owned by the handle                          */
     void *comm_stream;      /* cudaStream_t for halo exchange; NULL = owned by the handle   */
+    int32_t transport;      /* HEAT1D_TRANSPORT_* for the K2 schedule of several slabs; default
+                               P2P, which create turns into NCCL (on every rank) if any rank
+                               cannot map its neighbours' memory                            */
 } heat1d_opts;
 
 /* Read-only facts about a handle (heat1d_info). */
@@ -118,6 +129,8 @@ typedef struct {
     int32_t resident;       /* 1 if runs use the register-resident kernel K6                */
     int32_t resident_warps; /* warps of the last K6 launch                                  */
     int64_t stream_windows; /* light-cone windows of the last heat1d_solve_host (0: plain)  */
+    int32_t transport;      /* HEAT1D_TRANSPORT_* in use (after create's fallback)          */
+    int32_t reserved0;
 } heat1d_info_t;
 
 /* Exchange plan of one rank (pure host logic; usable without a GPU).  Offsets

@@ -35,6 +35,12 @@ namespace {
 struct Slab {
     int64_t first = 0, count = 0;
     double *buf[2] = {nullptr, nullptr};  // base of each padded buffer
+    // transport P2P: this slab's two exchange-index words (side 0 = left pad, +32 = right
+    // pad), where its new edge strips go in the neighbours' buffers (indexed by buffer),
+    // and the neighbours' words for those pads
+    unsigned *flags = nullptr;
+    double *put_left[2] = {nullptr, nullptr}, *put_right[2] = {nullptr, nullptr};
+    unsigned *nflag_left = nullptr, *nflag_right = nullptr;
 };
 
 thread_local std::string g_create_error;
@@ -79,6 +85,13 @@ struct heat1d_s {
     unsigned long long *win_absmax = nullptr;
     int64_t win_absmax_n = 0;
     int64_t stream_windows = 0;  // windows of the last heat1d_solve_host (0 = plain sequence)
+    // transport P2P (several slabs): exchange-index words of this handle's slabs, the
+    // neighbour ranks' allocations mapped over CUDA IPC, and the next exchange index
+    int transport = HEAT1D_TRANSPORT_NCCL;
+    unsigned *xflags = nullptr;
+    void *peer_alloc[2] = {nullptr, nullptr}, *peer_flags[2] = {nullptr, nullptr};  // [0] left, [1] right
+    bool peer_open[4] = {false, false, false, false};
+    unsigned xg = 0;
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     ncclComm_t nccl = nullptr;
     void *alloc = nullptr;
@@ -341,12 +354,35 @@ int run_passes(heat1d_t h, int64_t nt) {
             // B[T, n-T), K3 writes B[0,T) and B[n-T, n): disjoint; both read A.
             CK(cudaEventRecord(h->ev_ready, h->stream));
             CK(cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
-            int rc = exchange(h, Tp);
-            if (rc) return rc;
-            for (const Slab &s : h->slabs) {
-                CK(heat1d::launch_edges(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp, h->q,
-                                        heat1d::scale_of(h->r, Tp), h->comm));
-                h->launches++;
+            int rc = HEAT1D_OK;
+            if (h->transport == HEAT1D_TRANSPORT_P2P) {
+                // K3p: wait for the ghosts of index xg, update the strips, put them straight
+                // into the neighbours' pads of B with index xg+1
+                if (done == 0) {
+                    h->xg += 1;  // skip one index at every run boundary (slot-reuse safety, §8)
+                    for (const Slab &s : h->slabs) {
+                        CK(heat1d::launch_push_edges(cell0(h, s, h->cur), s.count, h->T, h->xg,
+                                                     s.put_left[h->cur], s.put_right[h->cur], s.nflag_left,
+                                                     s.nflag_right, h->comm));
+                        h->launches++;
+                    }
+                }
+                for (const Slab &s : h->slabs) {
+                    CK(heat1d::launch_edges_put(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp,
+                                                h->q, heat1d::scale_of(h->r, Tp), s.flags, h->xg,
+                                                s.put_left[h->cur ^ 1], s.put_right[h->cur ^ 1], s.nflag_left,
+                                                s.nflag_right, h->comm));
+                    h->launches++;
+                }
+                h->xg += 1;
+            } else {
+                rc = exchange(h, Tp);
+                if (rc) return rc;
+                for (const Slab &s : h->slabs) {
+                    CK(heat1d::launch_edges(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp, h->q,
+                                            heat1d::scale_of(h->r, Tp), h->comm));
+                    h->launches++;
+                }
             }
             CK(cudaEventRecord(h->ev_halo, h->comm));
             for (const Slab &s : h->slabs) {
@@ -471,6 +507,98 @@ int setup_multi_resident(heat1d_t h, bool local_fits) {
     return HEAT1D_OK;
 }
 
+// Transport P2P: exchange-index words for every slab, and the addresses K3p puts its
+// strips to -- the other virtual slabs' buffers, or the neighbour ranks' allocations
+// opened from CUDA IPC handles all-gathered over NCCL (lazy peer access: NVLink stores).
+int setup_p2p(heat1d_t h, int64_t nx, int64_t np) {
+    const int ns = (int)h->slabs.size();
+    const size_t fbytes = (size_t)ns * 64 * sizeof(unsigned);
+    CK(cudaMalloc(&h->xflags, fbytes < 256 ? 256 : fbytes));
+    CK(cudaMemset(h->xflags, 0, fbytes < 256 ? 256 : fbytes));
+    for (int g = 0; g < ns; ++g) h->slabs[g].flags = h->xflags + (size_t)g * 64;
+    if (h->nranks == 1) {
+        for (int g = 0; g < ns; ++g) {
+            Slab &s = h->slabs[g];
+            const Slab &L = h->slabs[(g - 1 + ns) % ns], &R = h->slabs[(g + 1) % ns];
+            for (int b = 0; b < 2; ++b) {
+                s.put_left[b] = cell0(h, L, b) + L.count;  // L's right pad
+                s.put_right[b] = cell0(h, R, b) - h->T;    // R's left pad
+            }
+            s.nflag_left = L.flags + 32;
+            s.nflag_right = R.flags;
+        }
+        return HEAT1D_OK;
+    }
+    const int G = h->nranks;
+    cudaIpcMemHandle_t mine[2];
+    CK(cudaIpcGetMemHandle(&mine[0], h->alloc));
+    CK(cudaIpcGetMemHandle(&mine[1], h->xflags));
+    const size_t hb = sizeof(mine);
+    char *dh = nullptr;
+    CK(cudaMalloc(&dh, (size_t)G * hb));
+    CK(cudaMemcpy(dh + (size_t)h->rank * hb, mine, hb, cudaMemcpyHostToDevice));
+    NK(ncclAllGather(dh + (size_t)h->rank * hb, dh, hb, ncclChar, h->nccl, h->comm));
+    std::vector<cudaIpcMemHandle_t> all((size_t)G * 2);
+    CK(cudaMemcpyAsync(all.data(), dh, (size_t)G * hb, cudaMemcpyDeviceToHost, h->comm));
+    CK(cudaStreamSynchronize(h->comm));
+    const int nbr[2] = {(h->rank - 1 + G) % G, (h->rank + 1) % G};
+    int ok = 1;  // every rank must map both neighbours, else all fall back to NCCL
+    for (int side = 0; side < 2 && ok; ++side) {
+        if (side == 1 && nbr[1] == nbr[0]) {  // G = 2: one peer on both sides
+            h->peer_alloc[1] = h->peer_alloc[0];
+            h->peer_flags[1] = h->peer_flags[0];
+            break;
+        }
+        for (int k = 0; k < 2 && ok; ++k) {
+            void **dst = k == 0 ? &h->peer_alloc[side] : &h->peer_flags[side];
+            if (cudaIpcOpenMemHandle(dst, all[(size_t)nbr[side] * 2 + k], cudaIpcMemLazyEnablePeerAccess) ==
+                cudaSuccess)
+                h->peer_open[side * 2 + k] = true;
+            else
+                ok = 0;
+        }
+    }
+    cudaGetLastError();
+    int *dok = reinterpret_cast<int *>(dh);  // (handles already copied out)
+    CK(cudaMemcpy(dok, &ok, sizeof ok, cudaMemcpyHostToDevice));
+    NK(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, h->nccl, h->comm));
+    CK(cudaMemcpyAsync(&ok, dok, sizeof ok, cudaMemcpyDeviceToHost, h->comm));
+    CK(cudaStreamSynchronize(h->comm));
+    if (!ok) {  // no peer mapping somewhere: the NCCL transport for everyone
+        for (int i = 0; i < 4; ++i)
+            if (h->peer_open[i]) cudaIpcCloseMemHandle(i % 2 == 0 ? h->peer_alloc[i / 2] : h->peer_flags[i / 2]);
+        for (int i = 0; i < 4; ++i) h->peer_open[i] = false;
+        h->peer_alloc[0] = h->peer_alloc[1] = h->peer_flags[0] = h->peer_flags[1] = nullptr;
+        h->transport = HEAT1D_TRANSPORT_NCCL;
+        CK(cudaFree(dh));
+        return HEAT1D_OK;
+    }
+    Slab &s = h->slabs[0];
+    for (int side = 0; side < 2; ++side) {
+        int64_t f = 0, c = 0;
+        partition(nx, np, G, nbr[side], &f, &c);
+        const int64_t len = round_up(c + 2 * h->pad, 32);  // the neighbour's buffer layout (same T)
+        double *base = static_cast<double *>(h->peer_alloc[side]);
+        for (int b = 0; b < 2; ++b) {
+            double *c0 = base + (size_t)b * len + h->pad;
+            if (side == 0)
+                s.put_left[b] = c0 + c;  // left rank's right pad
+            else
+                s.put_right[b] = c0 - h->T;  // right rank's left pad
+        }
+        if (side == 0)
+            s.nflag_left = static_cast<unsigned *>(h->peer_flags[0]) + 32;
+        else
+            s.nflag_right = static_cast<unsigned *>(h->peer_flags[1]);
+    }
+    // barrier: every rank's words are zeroed and mapped before any rank's first put
+    CK(cudaDeviceSynchronize());
+    NK(ncclAllReduce(dh, dh, 1, ncclInt32, ncclMin, h->nccl, h->comm));
+    CK(cudaStreamSynchronize(h->comm));
+    CK(cudaFree(dh));
+    return HEAT1D_OK;
+}
+
 int guard(heat1d_t h) {
     if (!h) return set_error(nullptr, HEAT1D_EINVAL, "NULL handle");
     if (h->poisoned) return h->poisoned;
@@ -499,6 +627,7 @@ void heat1d_opts_default(heat1d_opts *o) {
     o->blocking = 1;
     o->use_graphs = 1;
     o->resident = -1;
+    o->transport = HEAT1D_TRANSPORT_P2P;  // falls back to NCCL at create if peers cannot be mapped
 }
 
 int heat1d_version(void) { return HEAT1D_VERSION; }
@@ -597,6 +726,8 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     if (o.virtual_slabs < 1) return set_error(nullptr, HEAT1D_EINVAL, "virtual_slabs must be >= 1");
     if (o.virtual_slabs > 1 && o.nranks > 1)
         return set_error(nullptr, HEAT1D_EUNSUPPORTED, "virtual_slabs > 1 needs nranks == 1");
+    if (o.transport != HEAT1D_TRANSPORT_NCCL && o.transport != HEAT1D_TRANSPORT_P2P)
+        return set_error(nullptr, HEAT1D_EINVAL, "bad transport");
     if (o.T < 0 || o.T > HEAT1D_T_MAX) return set_error(nullptr, HEAT1D_EINVAL, "T must be in 0..%d", HEAT1D_T_MAX);
     const int G = o.virtual_slabs > 1 ? o.virtual_slabs : o.nranks;
     if (o.kernel == HEAT1D_KERNEL_NAIVE && G > 1)
@@ -630,7 +761,8 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     // Multi-rank runs do not capture NCCL calls into CUDA graphs: NCCL sets up its p2p
     // connections lazily (cudaMalloc/IPC, illegal under capture), and a pass there is long
     // (C4 at G=8: ~1.3 ms) next to its ~3 launches.
-    h->use_graphs = o.use_graphs != 0 && o.nranks == 1;
+    h->use_graphs = o.use_graphs != 0 && o.nranks == 1 && o.transport != HEAT1D_TRANSPORT_P2P;
+    h->transport = o.transport;  // (P2P pass arguments carry exchange indices: never replayed)
     h->ops = (o.mode == HEAT1D_MODE_FAST || is_pow2(r) || r == 0.0) ? 3 : 4;
     // r == 0: fma(0, t, b) == b + 0*t == b for finite t (identity either way)
     // Fast mode works on the scaled state v = u / r^t (stencil.cuh, DESIGN.md §3 c21): 1 DP op per
@@ -672,6 +804,10 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     int T = o.T > 0 ? o.T : auto_T(h->ops_fast ? h->ops_fast : h->ops);
     if (o.kernel == HEAT1D_KERNEL_NAIVE) T = 1;
     if (T > mslab) T = (int)mslab;  // a slab must hold its own halo
+    if (o.transport == HEAT1D_TRANSPORT_P2P && G > 1) {
+        if (mslab < 2) return set_error(nullptr, HEAT1D_EINVAL, "transport p2p needs slabs of >= 2 cells");
+        if (T > mslab / 2) T = (int)(mslab / 2);  // K3p's two strips must not overlap
+    }
     // K6 across ranks (one slab per rank): every rank must agree, decided after NCCL init
     bool res_multi_local = false;
     const bool res_ok = ((G == 1) || (o.nranks > 1 && o.virtual_slabs == 1)) && o.kernel == HEAT1D_KERNEL_AUTO &&
@@ -793,6 +929,13 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
                 set_error(nullptr, HEAT1D_EUNSUPPORTED, "a rank's slab does not fit the resident kernel");
                 return bail(HEAT1D_EUNSUPPORTED);
             }
+        }
+    }
+    if (h->transport == HEAT1D_TRANSPORT_P2P && h->multi() && !h->resident) {
+        int rc = setup_p2p(h, nx, np);
+        if (rc) {
+            set_error(nullptr, rc, "transport p2p setup: %s", h->last_error.c_str());
+            return bail(rc);
         }
     }
     if (h->resident && h->nranks == 1 && getenv("HEAT1D_K6_MAILBOX") && atoi(getenv("HEAT1D_K6_MAILBOX")) == 1) {
@@ -1111,6 +1254,7 @@ int heat1d_info(heat1d_t h, heat1d_info_t *info) {
     info->resident = h->resident ? 1 : 0;
     info->resident_warps = h->res_warps;
     info->stream_windows = h->stream_windows;
+    info->transport = h->transport;
     return HEAT1D_OK;
 }
 
@@ -1155,6 +1299,9 @@ int heat1d_destroy(heat1d_t h) {
     if (h->mbox_ipc_left) cudaIpcCloseMemHandle(h->mbox_left);
     if (h->mbox_ipc_right) cudaIpcCloseMemHandle(h->mbox_right);
     if (h->mbox) cudaFree(h->mbox);
+    for (int i = 0; i < 4; ++i)
+        if (h->peer_open[i]) cudaIpcCloseMemHandle(i % 2 == 0 ? h->peer_alloc[i / 2] : h->peer_flags[i / 2]);
+    if (h->xflags) cudaFree(h->xflags);
     if (h->win_absmax) cudaFree(h->win_absmax);
     for (int i = 0; i < 2; ++i) {
         if (h->ev_in[i]) cudaEventDestroy(h->ev_in[i]);

@@ -756,6 +756,101 @@ cudaError_t launch_edges(int ops, const double *A, double *B, int64_t n, int T, 
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ K3p
+// K3 fused with the halo exchange over peer memory (transport HEAT1D_TRANSPORT_P2P):
+// block 0 waits until its left ghost pad of A holds exchange index g (system-scope
+// acquire on the flag its left neighbour releases), advances the strip [0,T) T steps,
+// writes it to B AND straight into the left neighbour's right pad of B (remote stores
+// over NVLink, or plain stores for a slab on the same GPU), then releases the
+// neighbour's flag with g+1; block 1 mirrors this for [n-T,n) and the right
+// neighbour.  No NCCL call, host round trip or extra kernel sits between the edge
+// update and the data's arrival at the neighbour (PAPER.md:73's ghost exchange).
+__device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_sys_u32(unsigned *p, unsigned v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int OPS>
+__global__ void __launch_bounds__(96) k3_edges_put(const double *__restrict__ A, double *__restrict__ B, int64_t n,
+                                                   int T, double r, double scale, const unsigned *my_flags,
+                                                   unsigned g, double *put_left, double *put_right,
+                                                   unsigned *flag_left, unsigned *flag_right) {
+    __shared__ double w[2][3 * 128];
+    const int side = blockIdx.x;  // 0: [0,T) <- left pad; 1: [n-T,n) <- right pad
+    if (threadIdx.x == 0) {
+        const unsigned *f = my_flags + side * 32;
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire_sys_u32(f) < g + 1) {
+            if (globaltimer_ns() - t0 > HEAT1D_WAIT_NS) __trap();
+        }
+    }
+    __syncthreads();
+    const int64_t base = (side == 0) ? -(int64_t)T : n - 2 * (int64_t)T;
+    const int len = 3 * T;
+    for (int i = threadIdx.x; i < len; i += blockDim.x) w[0][i] = __ldcv(A + base + i);  // pads: peer-written
+    __syncthreads();
+    int cur = 0;
+    for (int s = 0; s < T; ++s) {
+        const int lo = s + 1, hi = len - 1 - s;
+        for (int i = lo + threadIdx.x; i < hi; i += blockDim.x)
+            w[cur ^ 1][i] = eq2<OPS>(w[cur][i - 1], w[cur][i], w[cur][i + 1], r);
+        cur ^= 1;
+        __syncthreads();
+    }
+    double *put = side == 0 ? put_left : put_right;
+    for (int i = threadIdx.x; i < T; i += blockDim.x) {
+        double x = w[cur][T + i];
+        if constexpr (ops_scaled(OPS)) x = __dmul_rn(x, scale);
+        B[base + T + i] = x;
+        put[i] = x;
+    }
+    __syncthreads();  // every thread's put precedes thread 0's (cumulative) release
+    if (threadIdx.x == 0) st_release_sys_u32(side == 0 ? flag_left : flag_right, g + 2);
+}
+
+cudaError_t launch_edges_put(int ops, const double *A, double *B, int64_t n, int T, double q, double scale,
+                             const unsigned *my_flags, unsigned g, double *put_left, double *put_right,
+                             unsigned *flag_left, unsigned *flag_right, cudaStream_t st) {
+    if (T < 1 || T > 128 || n < 2 * (int64_t)T) return cudaErrorInvalidValue;
+#define K3P(o) k3_edges_put<o><<<2, 96, 0, st>>>(A, B, n, T, q, scale, my_flags, g, put_left, put_right, flag_left, flag_right)
+    switch (ops) {
+        case 4: K3P(4); break;
+        case 3: K3P(3); break;
+        case 2: K3P(2); break;
+        case 1: K3P(1); break;
+        default: return cudaErrorInvalidValue;
+    }
+#undef K3P
+    return cudaGetLastError();
+}
+
+// Start of a run (transport P2P): push this slab's current edge cells [0,T) and [n-T,n)
+// into the neighbours' pads of the same buffer and release their flags with g+1 (the
+// index the run's first pass waits for).  Also covers a new initial state and a run
+// whose first pass is deeper than the previous run's tail pass.
+__global__ void __launch_bounds__(128) k_push_edges(const double *__restrict__ A, int64_t n, int T, unsigned g,
+                                                   double *put_left, double *put_right, unsigned *flag_left,
+                                                   unsigned *flag_right) {
+    const int side = blockIdx.x;
+    const double *src = side == 0 ? A : A + n - T;
+    double *dst = side == 0 ? put_left : put_right;
+    for (int i = threadIdx.x; i < T; i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_sys_u32(side == 0 ? flag_left : flag_right, g + 1);
+}
+
+cudaError_t launch_push_edges(const double *A, int64_t n, int T, unsigned g, double *put_left, double *put_right,
+                              unsigned *flag_left, unsigned *flag_right, cudaStream_t st) {
+    if (T < 1 || n < T) return cudaErrorInvalidValue;
+    k_push_edges<<<2, 128, 0, st>>>(A, n, T, g, put_left, put_right, flag_left, flag_right);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ K4
 __global__ void k4_wrap_fill(double *A, int64_t n, int64_t pad) {
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < pad; j += (int64_t)gridDim.x * blockDim.x) {

@@ -65,6 +65,17 @@ cudaError_t launch_naive(int ops, const double *A, double *B, int64_t n, double 
 cudaError_t launch_edges(int ops, const double *A, double *B, int64_t n, int T, double q, double scale,
                          cudaStream_t st);
 
+// K3p: K3 fused with a peer-memory halo put (kernels.cu).  my_flags: this slab's two
+// exchange-index words (side 0 at +0, side 1 at +32); put_left/right: where the new
+// left/right strips go in the neighbours' B (their right/left pads); flag_left/right:
+// the neighbours' words for those pads.  Waits for index g, releases g+1.
+cudaError_t launch_edges_put(int ops, const double *A, double *B, int64_t n, int T, double q, double scale,
+                             const unsigned *my_flags, unsigned g, double *put_left, double *put_right,
+                             unsigned *flag_left, unsigned *flag_right, cudaStream_t st);
+// Push A[0,T) / A[n-T,n) into the neighbours' pads and release their flags with g+1.
+cudaError_t launch_push_edges(const double *A, int64_t n, int T, unsigned g, double *put_left, double *put_right,
+                              unsigned *flag_left, unsigned *flag_right, cudaStream_t st);
+
 // K4: fill `pad` ghost cells on each side of a single-slab ring, modularly.
 cudaError_t launch_wrap_fill(double *A, int64_t n, int64_t pad, cudaStream_t st);
 

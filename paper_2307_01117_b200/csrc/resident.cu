@@ -209,7 +209,9 @@ __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, const 
         const unsigned *Lf = lrem ? mbox_flag(mb.self, 0) : flags + s.left;
         const unsigned *Rf = rrem ? mbox_flag(mb.self, 1) : flags + s.right;
         const unsigned Lt = !doL ? 0u : lrem ? g + 1 : p + 1, Rt = !doR ? 0u : rrem ? g + 1 : p + 1;
+        const unsigned long long t0 = globaltimer_ns();
         while (!__all_sync(0xffffffffu, ld_relaxed_sys(Lf) >= Lt && ld_relaxed_sys(Rf) >= Rt)) {
+            if (globaltimer_ns() - t0 > HEAT1D_WAIT_NS) __trap();  // a neighbour rank is gone
         }
         if (doL) (void)ld_acquire_sys(Lf);
         if (doR) (void)ld_acquire_sys(Rf);

@@ -47,4 +47,14 @@ __device__ __forceinline__ double eq2(double a, double b, double c, double q) {
     }
 }
 
+// Cross-rank waits (peer-memory flags) must not hang a process forever if a neighbour
+// rank died or diverged: after HEAT1D_WAIT_NS of polling the kernel traps (the CUDA
+// error poisons the handle; the caller sees HEAT1D_ECUDA instead of a hang).
+constexpr unsigned long long HEAT1D_WAIT_NS = 30ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 }  // namespace heat1d

@@ -53,6 +53,7 @@ class Opts(ctypes.Structure):
         ("resident", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
         ("comm_stream", ctypes.c_void_p),
+        ("transport", ctypes.c_int32),
     ]
 
 
@@ -84,6 +85,8 @@ class Info(ctypes.Structure):
         ("resident", ctypes.c_int32),
         ("resident_warps", ctypes.c_int32),
         ("stream_windows", ctypes.c_int64),
+        ("transport", ctypes.c_int32),
+        ("reserved0", ctypes.c_int32),
     ]
 
 
@@ -221,7 +224,8 @@ class Heat1D:
                  mode: str = "matched", denominator: str = "dx2", allow_unstable: bool = False,
                  rank: int = 0, nranks: int = 1, nccl_id: Optional[bytes] = None, virtual_slabs: int = 1,
                  kernel: str = "auto", device: int = -1, stream=None, comm_stream=None,
-                 blocking: bool = True, use_graphs: bool = True, resident: Optional[bool] = None):
+                 blocking: bool = True, use_graphs: bool = True, resident: Optional[bool] = None,
+                 transport: str = "p2p"):
         self._lib = load()
         o = default_opts()
         o.device = device
@@ -241,6 +245,7 @@ class Heat1D:
         o.resident = -1 if resident is None else (1 if resident else 0)
         o.stream = _stream_ptr(stream)
         o.comm_stream = _stream_ptr(comm_stream)
+        o.transport = {"nccl": 0, "p2p": 1}[transport]
         h = ctypes.c_void_p()
         st = self._lib.heat1d_create(ctypes.byref(h), nx, np_, nt, float(k), float(dt), float(dx), ctypes.byref(o))
         _check(st, None)

@@ -292,14 +292,40 @@ def test_graph_replay(h1, vs):
 
 @pytest.mark.parametrize("G", [2, 3, 4, 8])
 @pytest.mark.parametrize("T", [1, 4, 8, 12, 32, 64])
-def test_virtual_slabs_multi_gpu_schedule(h1, G, T):
-    """The multi-GPU schedule (exchange || interior, then edges) with the
-    transport replaced by device copies between G slabs on one GPU."""
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_virtual_slabs_multi_gpu_schedule(h1, G, T, transport):
+    """The multi-GPU schedule with G slabs on one GPU: exchange || interior, then edges,
+    with the transport replaced by device copies ("nccl"), or the fused K3p that puts its
+    new strips into the neighbour slabs' pads and releases their exchange-index words
+    ("p2p": the same kernels and protocol as across ranks, peers = other slabs)."""
     nx, np_ = 12_289, 8
     nt = 3 * T + 1
     u0 = synth.uniform(G * 100 + T, 0, nx * np_, -1.0, 1.0)
     want = oracle.run(u0, 0.4, nt)
-    assert_bitwise(gpu_run(h1, u0, nx, np_, nt, 0.4, T=T, virtual_slabs=G), want, "G=%d T=%d" % (G, T))
+    assert_bitwise(gpu_run(h1, u0, nx, np_, nt, 0.4, T=T, virtual_slabs=G, transport=transport), want,
+                   "G=%d T=%d %s" % (G, T, transport))
+
+
+@pytest.mark.parametrize("G", [2, 5])
+def test_p2p_transport_runs_and_modes(h1, G):
+    """Transport p2p over consecutive runs (run-boundary re-push after a shallow tail pass,
+    exchange indices that keep growing), a new initial state, and fast mode."""
+    nx, np_, T = 20_011, 4, 16
+    u0 = synth.uniform(G + 3, 0, nx * np_, -1.0, 1.0)
+    with h1.Heat1D(nx, np_, 0, 0.4, 1.0, 1.0, T=T, virtual_slabs=G, transport="p2p") as h:
+        h.set_initial(u0)
+        want = u0
+        for nt in (2 * T + 5, T, 3, 1, 2 * T):
+            h.run(nt)
+            want = oracle.run(want, 0.4, nt)
+            assert_bitwise(h.get(), want, "p2p G=%d +%d" % (G, nt))
+        h.set_initial(u0)
+        h.run(T + 1)
+        assert_bitwise(h.get(), oracle.run(u0, 0.4, T + 1), "p2p after set_initial")
+    with h1.Heat1D(nx, np_, 0, 0.5, 1.0, 1.0, T=T, virtual_slabs=G, transport="p2p", mode="fast") as h:
+        h.set_initial(u0)
+        h.run(77)
+        assert np.max(np.abs(h.get() - oracle.run(u0, 0.5, 77))) <= fast_bound(u0, 77)
 
 
 def test_virtual_slabs_small_slabs(h1):
@@ -551,12 +577,14 @@ def test_c4_first_100_steps_windows(h1):
         got[a] = out[torch.from_numpy(idx).cuda()].cpu().numpy()
         w = oracle.window(C4.u0(a - nt, 512 + 2 * nt), nt, r)
         assert_bitwise(got[a], w, "C4 window %d" % a)
-    with h1.Heat1D(C4.nx, C4.np, nt, C4.k, C4.dt, C4.dx, virtual_slabs=8) as h:
-        h.init_uniform(C4.seed, C4.lo, C4.hi)
-        h.run()
-        out2 = torch.empty(N, dtype=torch.float64, device="cuda")
-        h.get(out2)
-    assert torch.equal(out, out2)
+    for transport in ("nccl", "p2p"):
+        with h1.Heat1D(C4.nx, C4.np, nt, C4.k, C4.dt, C4.dx, virtual_slabs=8, transport=transport) as h:
+            h.init_uniform(C4.seed, C4.lo, C4.hi)
+            h.run()
+            out2 = torch.empty(N, dtype=torch.float64, device="cuda")
+            h.get(out2)
+        assert torch.equal(out, out2), transport
+        del out2
 
 
 @pytest.mark.parametrize("mode", ["matched", "fast"])
