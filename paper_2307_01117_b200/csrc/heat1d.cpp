@@ -825,8 +825,8 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
         int coop = 0;
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
         const bool fits = coop && n0 <= heat1d::resident_capacity(Tr, h->num_sms) && n0 >= Tr &&
-                          heat1d::resident_fits(h->ops, n0, Tr, h->num_sms) &&
-                          (!h->ops_fast || heat1d::resident_fits(h->ops_fast, n0, Tr, h->num_sms));
+                          heat1d::resident_fits(h->ops, n0, Tr, h->num_sms, G > 1) &&
+                          (!h->ops_fast || heat1d::resident_fits(h->ops_fast, n0, Tr, h->num_sms, G > 1));
         cudaGetLastError();
         if (fits && G > 1) {
             res_multi_local = true;  // tentatively: T = Tr; agreed on below
@@ -938,7 +938,9 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
             return bail(rc);
         }
     }
-    if (h->resident && h->nranks == 1 && getenv("HEAT1D_K6_MAILBOX") && atoi(getenv("HEAT1D_K6_MAILBOX")) == 1) {
+    if (h->resident && h->nranks == 1 && getenv("HEAT1D_K6_MAILBOX") && atoi(getenv("HEAT1D_K6_MAILBOX")) == 1 &&
+        heat1d::resident_fits(h->ops, h->N, h->T, h->num_sms, true) &&
+        (!h->ops_fast || heat1d::resident_fits(h->ops_fast, h->N, h->T, h->num_sms, true))) {
         // test knob: route the single rank's wrap through its own mailbox (the multi-rank protocol)
         if (cudaMalloc(&h->mbox, heat1d::MBOX_BYTES) != cudaSuccess ||
             cudaMemset(h->mbox, 0, heat1d::MBOX_BYTES) != cudaSuccess) {

@@ -101,7 +101,7 @@ struct MboxArgs {
 
 // K6: whole nt-step solve of a single-slab ring held in registers (resident.cu).
 int64_t resident_capacity(int T, int num_sms);
-bool resident_fits(int ops, int64_t n, int T, int num_sms);  // plan + co-residency check
+bool resident_fits(int ops, int64_t n, int T, int num_sms, bool mbox = false);  // plan + co-residency
 size_t resident_scratch_bytes(int T, int num_sms);
 cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
                             double r, void *scratch, int num_sms, cudaStream_t st, int *warps_out,

@@ -256,10 +256,12 @@ __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, const 
 
 }  // namespace
 
-template <int V, int OPS, int SPW, bool EARLY>
+// MB: the cross-rank mailbox code is compiled in (only then: it costs ~30 registers).
+template <int V, int OPS, int SPW, bool EARLY, bool MB = false>
 __global__ void __launch_bounds__(256)
 k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t nt, double r,
-            double rr, double *__restrict__ edges, unsigned *__restrict__ flags, int Wt, int sync, MboxArgs mb) {
+            double rr, double *__restrict__ edges, unsigned *__restrict__ flags, int Wt, int sync, MboxArgs mb_in) {
+    const MboxArgs mb = MB ? mb_in : MboxArgs{};
     extern __shared__ __align__(16) double srow[];
     const int lane = threadIdx.x & 31;
     const int wib = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);  // warp-uniform for the compiler
@@ -357,7 +359,13 @@ int res_sync() {
     return e ? atoi(e) : 0;
 }
 
-const void *res_fn(int ops, int spw, int rv) {
+const void *res_fn(int ops, int spw, int rv, bool mbox = false) {
+    if (mbox) {  // SPW = 1, early shuffles, mailbox code compiled in
+#define RFM(v) (ops == 4 ? (const void *)&k6_resident<v, 4, 1, true, true> : ops == 3 ? (const void *)&k6_resident<v, 3, 1, true, true> \
+                : ops == 2 ? (const void *)&k6_resident<v, 2, 1, true, true> : (const void *)&k6_resident<v, 1, 1, true, true>)
+        return rv == 49 ? RFM(49) : rv == 33 ? RFM(33) : RFM(17);
+#undef RFM
+    }
     const bool early = res_early() != 0;
 #define RF(v, o, s, e) (const void *)&k6_resident<v, o, s, e>
 #define RF_OPS(v, s, e) (ops == 4 ? RF(v, 4, s, e) : ops == 3 ? RF(v, 3, s, e) : ops == 2 ? RF(v, 2, s, e) : RF(v, 1, s, e))
@@ -418,7 +426,7 @@ bool res_plan(int ops, int64_t n, int T, int num_sms, ResPlan *p, bool mbox = fa
     const int64_t ns = p->wt * p->spw;
     if (n / ns < T || n / ns + (n % ns ? 1 : 0) + 2 * T > 32 * RV) return false;
     p->smem = (size_t)p->nw * p->spw * (32 * RV + 1) * sizeof(double);
-    const void *fn = res_fn(ops, p->spw, RV);
+    const void *fn = res_fn(ops, p->spw, RV, mbox);
     if (res_attr(fn) != cudaSuccess) return false;
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, (int)(p->nw * 32), p->smem) != cudaSuccess)
@@ -434,9 +442,9 @@ int64_t resident_capacity(int T, int num_sms) {
     return (int64_t)num_sms * (a > b ? a : b) * (32 * rv - 2 * T);
 }
 
-bool resident_fits(int ops, int64_t n, int T, int num_sms) {
+bool resident_fits(int ops, int64_t n, int T, int num_sms, bool mbox) {
     ResPlan p;
-    return res_plan(ops, n, T, num_sms, &p, false);
+    return res_plan(ops, n, T, num_sms, &p, mbox);
 }
 
 size_t resident_scratch_bytes(int T, int num_sms) {
@@ -462,7 +470,7 @@ cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int 
     if (getenv("HEAT1D_DEBUG"))
         fprintf(stderr, "[heat1d] K6 n=%lld T=%d spw=%d Wt=%d nw=%lld grid=%lld smem=%zu\n", (long long)n, T,
                 p.spw, Wt, (long long)p.nw, (long long)p.grid, p.smem);
-    return cudaLaunchCooperativeKernel(res_fn(ops, p.spw, p.rv), dim3((unsigned)p.grid), dim3((unsigned)(p.nw * 32)),
+    return cudaLaunchCooperativeKernel(res_fn(ops, p.spw, p.rv, mb.on != 0), dim3((unsigned)p.grid), dim3((unsigned)(p.nw * 32)),
                                        args, p.smem, st);
 }
 
