@@ -107,6 +107,9 @@ typedef struct {
     int32_t transport;      /* HEAT1D_TRANSPORT_* for the K2 schedule of several slabs; default
                                P2P, which create turns into NCCL (on every rank) if any rank
                                cannot map its neighbours' memory                            */
+    double *dev_buf;        /* optional caller-owned device memory for the state (e.g. a torch
+                               tensor): >= heat1d_buffer_len(nx, np, opts) doubles, 256-byte
+                               aligned, outliving the handle; NULL = the handle cudaMallocs   */
 } heat1d_opts;
 
 /* Read-only facts about a handle (heat1d_info). */

@@ -95,6 +95,7 @@ struct heat1d_s {
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     ncclComm_t nccl = nullptr;
     void *alloc = nullptr;
+    bool own_alloc = true;  // false: opts.dev_buf (caller-owned, e.g. a torch tensor)
 
     // CUDA graphs of whole run(nt) pass sequences, keyed by (nt, starting buffer)
     struct Graph {
@@ -531,8 +532,14 @@ int setup_p2p(heat1d_t h, int64_t nx, int64_t np) {
     }
     const int G = h->nranks;
     cudaIpcMemHandle_t mine[2];
-    CK(cudaIpcGetMemHandle(&mine[0], h->alloc));
-    CK(cudaIpcGetMemHandle(&mine[1], h->xflags));
+    memset(mine, 0, sizeof mine);
+    // a caller-owned opts.dev_buf may be a sub-allocation (torch's caching allocator): its
+    // IPC handle would map the containing block, so such a rank votes for NCCL below
+    int ok = h->own_alloc ? 1 : 0;
+    if (ok && (cudaIpcGetMemHandle(&mine[0], h->alloc) != cudaSuccess ||
+               cudaIpcGetMemHandle(&mine[1], h->xflags) != cudaSuccess))
+        ok = 0;
+    cudaGetLastError();
     const size_t hb = sizeof(mine);
     char *dh = nullptr;
     CK(cudaMalloc(&dh, (size_t)G * hb));
@@ -542,7 +549,8 @@ int setup_p2p(heat1d_t h, int64_t nx, int64_t np) {
     CK(cudaMemcpyAsync(all.data(), dh, (size_t)G * hb, cudaMemcpyDeviceToHost, h->comm));
     CK(cudaStreamSynchronize(h->comm));
     const int nbr[2] = {(h->rank - 1 + G) % G, (h->rank + 1) % G};
-    int ok = 1;  // every rank must map both neighbours, else all fall back to NCCL
+    // every rank must map both neighbours, else all fall back to NCCL; a handle of zeros
+    // (a neighbour that voted no) fails to open here too
     for (int side = 0; side < 2 && ok; ++side) {
         if (side == 1 && nbr[1] == nbr[0]) {  // G = 2: one peer on both sides
             h->peer_alloc[1] = h->peer_alloc[0];
@@ -862,11 +870,21 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     h->count = 0;
     for (auto &s : h->slabs) h->count += s.count;
 
-    cudaError_t e = cudaMalloc(&h->alloc, (size_t)total * sizeof(double));
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        set_error(nullptr, HEAT1D_ENOMEM, "cudaMalloc(%lld bytes): %s", (long long)total * 8, cudaGetErrorString(e));
-        return bail(HEAT1D_ENOMEM);
+    if (o.dev_buf) {  // caller-owned device memory (>= heat1d_buffer_len doubles, 256-B aligned)
+        if (reinterpret_cast<uintptr_t>(o.dev_buf) % 256) {
+            set_error(nullptr, HEAT1D_EINVAL, "dev_buf must be 256-byte aligned");
+            return bail(HEAT1D_EINVAL);
+        }
+        h->alloc = o.dev_buf;
+        h->own_alloc = false;
+    } else {
+        cudaError_t e = cudaMalloc(&h->alloc, (size_t)total * sizeof(double));
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            set_error(nullptr, HEAT1D_ENOMEM, "cudaMalloc(%lld bytes): %s", (long long)total * 8,
+                      cudaGetErrorString(e));
+            return bail(HEAT1D_ENOMEM);
+        }
     }
     double *p = static_cast<double *>(h->alloc);
     for (auto &s : h->slabs) {
@@ -1295,7 +1313,7 @@ int heat1d_destroy(heat1d_t h) {
     if (h->ev_halo) cudaEventDestroy(h->ev_halo);
     if (h->own_comm && h->comm) cudaStreamDestroy(h->comm);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
-    if (h->alloc) cudaFree(h->alloc);
+    if (h->alloc && h->own_alloc) cudaFree(h->alloc);
     if (h->res_scratch) cudaFree(h->res_scratch);
     if (h->absmax) cudaFree(h->absmax);
     if (h->mbox_ipc_left) cudaIpcCloseMemHandle(h->mbox_left);

@@ -54,6 +54,7 @@ class Opts(ctypes.Structure):
         ("stream", ctypes.c_void_p),
         ("comm_stream", ctypes.c_void_p),
         ("transport", ctypes.c_int32),
+        ("dev_buf", ctypes.c_void_p),
     ]
 
 
@@ -225,7 +226,7 @@ class Heat1D:
                  rank: int = 0, nranks: int = 1, nccl_id: Optional[bytes] = None, virtual_slabs: int = 1,
                  kernel: str = "auto", device: int = -1, stream=None, comm_stream=None,
                  blocking: bool = True, use_graphs: bool = True, resident: Optional[bool] = None,
-                 transport: str = "p2p"):
+                 transport: str = "p2p", dev_buf=None):
         self._lib = load()
         o = default_opts()
         o.device = device
@@ -246,6 +247,13 @@ class Heat1D:
         o.stream = _stream_ptr(stream)
         o.comm_stream = _stream_ptr(comm_stream)
         o.transport = {"nccl": 0, "p2p": 1}[transport]
+        self._dev_buf = dev_buf  # caller-owned state memory (torch tensor): kept alive with the handle
+        if dev_buf is not None:
+            ptr, n, _ = _data_ptr(dev_buf)
+            need = buffer_len(nx, np_, o)
+            if n < need:
+                raise ValueError("dev_buf holds %d doubles, the handle needs %d (buffer_len)" % (n, need))
+            o.dev_buf = ptr
         h = ctypes.c_void_p()
         st = self._lib.heat1d_create(ctypes.byref(h), nx, np_, nt, float(k), float(dt), float(dx), ctypes.byref(o))
         _check(st, None)

@@ -699,3 +699,31 @@ def test_ring_beyond_2pow32_cells(h1):
                 assert np.max(np.abs(got - want[a])) <= 1e-12 * nt, a
         del out
         torch.cuda.empty_cache()
+
+
+def test_caller_owned_device_memory(h1):
+    """opts.dev_buf: the state lives in a torch tensor the caller owns (PyTorch provides the
+    device memory; BASELINE.json north_star), single slab and virtual slabs, both modes."""
+    import torch
+    N, nt = 300_007, 50
+    u0 = synth.uniform(31, 0, N, -1.0, 1.0)
+    want = oracle.run(u0, 0.4, nt)
+    for kw in ({}, {"virtual_slabs": 3}, {"resident": False}, {"mode": "fast"}):
+        o = h1.default_opts()
+        o.virtual_slabs = kw.get("virtual_slabs", 1)
+        buf = torch.empty(h1.buffer_len(N, 1, o), dtype=torch.float64, device="cuda")
+        with h1.Heat1D(N, 1, nt, 0.4, 1.0, 1.0, dev_buf=buf, **kw) as h:
+            h.set_initial(u0)
+            h.run()
+            got = h.get()
+        if kw.get("mode") == "fast":
+            assert np.max(np.abs(got - want)) <= fast_bound(u0, nt)
+        else:
+            assert_bitwise(got, want, "dev_buf %r" % kw)
+    small = torch.empty(1000, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        h1.Heat1D(N, 1, nt, 0.4, 1.0, 1.0, dev_buf=small)
+    big = torch.empty(h1.buffer_len(N, 1, h1.default_opts()) + 1, dtype=torch.float64, device="cuda")
+    with pytest.raises(h1.Heat1DError) as ei:                # 8-byte offset: not 256-byte aligned
+        h1.Heat1D(N, 1, nt, 0.4, 1.0, 1.0, dev_buf=big[1:])
+    assert ei.value.status == 1
