@@ -312,11 +312,8 @@ int run_resident(heat1d_t h, int64_t nt) {
     h->launches++;
     if (h->prof) CK(cudaEventRecord(e1, h->stream));
     h->cur ^= 1;
-    if (h->nranks == 1) {
-        // keep the periodic pads of the new state valid (cheap; lets any path continue)
-        CK(heat1d::launch_wrap_fill(cell0(h, s, h->cur), s.count, h->pad, h->stream));
-        h->launches++;
-    }
+    // (no periodic pads to refresh: K6 reads its halos modularly and a resident handle never
+    // runs another kernel family)
     h->steps_done += nt;
     return HEAT1D_OK;
 }
@@ -1021,7 +1018,7 @@ static int select_fast_ops(heat1d_t h) {
 }
 
 static int after_initial(heat1d_t h) {
-    if (!h->multi()) {
+    if (!h->multi() && !h->resident) {
         const Slab &s = h->slabs[0];
         CK(heat1d::launch_wrap_fill(cell0(h, s, h->cur), s.count, h->pad, h->stream));
         h->launches++;
