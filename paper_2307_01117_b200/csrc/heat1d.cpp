@@ -822,10 +822,10 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
         if (G > 1) partition(nx, np, G, o.rank, &f0, &n0);
         // K6 period (halo refresh) <= 128; auto = 64 (V = 33 spans): half the exchanges of T = 32
         // for +32 % (C5) / +30 % (C2) measured (profiles/r01_k6_period_sync.jsonl)
-        // (matched 3/4-op forms: T = 128 with V = 49 spans, +11 % on C5/C2; the fast forms lose
-        // occupancy to V = 49's registers and stay at 64: profiles/r01_k6_period_v49.jsonl)
-        const int ops_k6 = h->ops_fast ? h->ops_fast : h->ops;
-        int Tr = o.T > 0 ? std::min(o.T, 128) : (ops_k6 >= 3 ? 128 : 64);
+        // (T = 64, V = 33 spans for every arithmetic form since the cross-rank mailbox code
+        // is compiled only where used: C5 matched 4114 vs 3216 GLUPS at T = 128 / V = 49;
+        // profiles/r01_k6_period_v.jsonl)
+        int Tr = o.T > 0 ? std::min(o.T, 128) : 64;
         if (Tr > mslab) Tr = (int)mslab;
         int coop = 0;
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);

@@ -336,7 +336,13 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
 
 namespace {
 // cells per lane: 17 for periods T <= 32, 33 for 32 < T <= 64, 49 up to 128 (span 32V >= own + 2T)
-int rv_of(int T) { return T > 64 ? 49 : T > 32 ? 33 : 17; }
+int rv_of(int T) {
+    if (const char *e = getenv("HEAT1D_K6_V")) {  // tuning knob: 17, 33 or 49 if the span holds 2T
+        const int v = atoi(e);
+        if ((v == 17 || v == 33 || v == 49) && 32 * v > 2 * T) return v;
+    }
+    return T > 64 ? 49 : T > 32 ? 33 : 17;
+}
 // warps per SM the register budget allows: V=17: ~100 regs (1 span/warp), ~156 (2 spans/warp);
 // V=33: ~128 regs (1 span/warp only)
 int max_wps(int rv, int spw) { return rv == 49 ? 9 : rv == 33 ? 15 : spw == 1 ? 20 : 12; }
