@@ -15,6 +15,7 @@
 // exchange done every T steps at depth T instead of every step at depth 1.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: named ranges for nsys/ncu timelines
 
 #include <cmath>
 #include <cstdarg>
@@ -131,6 +132,11 @@ int set_error(heat1d_t h, int status, const char *fmt, ...) {
         g_create_error = buf;
     return status;
 }
+
+struct NvtxRange {  // scoped NVTX range (no-op unless a profiler is attached)
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 int fail_cuda(heat1d_t h, cudaError_t e, const char *what, int line) {
     if (h) h->poisoned = HEAT1D_ECUDA;
@@ -319,6 +325,7 @@ int run_resident(heat1d_t h, int64_t nt) {
 }
 
 int run_passes(heat1d_t h, int64_t nt) {
+    NvtxRange range(h->resident ? "heat1d.run K6" : h->multi() ? "heat1d.run K2+exchange" : "heat1d.run K2");
     if (h->resident) return run_resident(h, nt);
     int64_t done = 0;
     while (done < nt) {
@@ -1018,6 +1025,15 @@ static int select_fast_ops(heat1d_t h) {
 }
 
 static int after_initial(heat1d_t h) {
+    if (h->multi() && h->nranks == 1 && getenv("HEAT1D_POISON_PADS") && atoi(getenv("HEAT1D_POISON_PADS")) == 1) {
+        // fault injection (tests): NaN in every ghost pad of both buffers -- any pad value
+        // read before the exchange refreshed it would poison the result
+        for (const Slab &s : h->slabs)
+            for (int b = 0; b < 2; ++b) {
+                CK(cudaMemsetAsync(s.buf[b], 0xff, (size_t)h->pad * 8, h->stream));
+                CK(cudaMemsetAsync(cell0(h, s, b) + s.count, 0xff, (size_t)h->pad * 8, h->stream));
+            }
+    }
     if (!h->multi() && !h->resident) {
         const Slab &s = h->slabs[0];
         CK(heat1d::launch_wrap_fill(cell0(h, s, h->cur), s.count, h->pad, h->stream));
@@ -1066,6 +1082,11 @@ int heat1d_run(heat1d_t h, int64_t nt) {
     if (rc) return rc;
     if (h->blocking) {
         CK(cudaStreamSynchronize(h->stream));
+        if (h->nccl) {  // a peer's failure surfaces asynchronously on the communicator
+            ncclResult_t ae = ncclSuccess;
+            NK(ncclCommGetAsyncError(h->nccl, &ae));
+            if (ae != ncclSuccess) return fail_nccl(h, ae, "ncclCommGetAsyncError", __LINE__);
+        }
         if (h->prof) {
             rc = prof_collect(h);
             if (rc) return rc;

@@ -727,3 +727,17 @@ def test_caller_owned_device_memory(h1):
     with pytest.raises(h1.Heat1DError) as ei:                # 8-byte offset: not 256-byte aligned
         h1.Heat1D(N, 1, nt, 0.4, 1.0, 1.0, dev_buf=big[1:])
     assert ei.value.status == 1
+
+
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_nan_poisoned_pads(h1, monkeypatch, transport):
+    """Fault injection: every ghost pad starts as NaN (HEAT1D_POISON_PADS=1); the exchange
+    must overwrite each pad before any kernel reads it, so the result stays bitwise exact."""
+    monkeypatch.setenv("HEAT1D_POISON_PADS", "1")
+    nx, np_, G = 30_011, 6, 3
+    u0 = synth.uniform(808, 0, nx * np_, -1.0, 1.0)
+    for T, nt in [(8, 2 * 8 + 3), (64, 64 + 1)]:
+        want = oracle.run(u0, 0.4, nt)
+        got = gpu_run(h1, u0, nx, np_, nt, 0.4, T=T, virtual_slabs=G, transport=transport)
+        assert np.all(np.isfinite(got))
+        assert_bitwise(got, want, "poisoned pads %s T=%d" % (transport, T))
