@@ -51,6 +51,19 @@ def parse():
     return p.parse_args()
 
 
+def fp64_peak():
+    """fp64 pipe peak in T lane-instructions/s: measured by tools/fp64_peak.cu on a B200 of this
+    pool (profiles/fp64_peak.json, best DADD rate), else derived from 148 SM x 64 lanes x 1.965 GHz."""
+    derived = SMS * FP64_LANES * SM_MHZ_MAX * 1e6 / 1e12
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            d = json.load(f)
+        best = max(r["dadd_tinst_s"] for r in d["results"])
+        return best, "measured (tools/fp64_peak.cu: independent DADD chains, profiles/fp64_peak.json)"
+    except Exception:
+        return derived, "derived: 148 SM x 64 fp64 lanes x 1.965 GHz"
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -211,7 +224,7 @@ def kernel_roofline(info, cfg, count, world, steps, k2_launches, k2_ms, ms, valu
     # 148 SM x 64 lanes x 1.965 GHz against its algorithmic fp64 instructions per update
     # (dp_ops; the scaled fast variants add one rescale DMUL per cell per pass)
     inst_per_upd = info["dp_ops"] + (1.0 / steps_per_pass if info["dp_ops"] <= 2 else 0.0)
-    pipe = SMS * FP64_LANES * SM_MHZ_MAX * 1e6 / 1e12        # T fp64 lane-instructions / s
+    pipe, pipe_kind = fp64_peak()                            # T fp64 lane-instructions / s
     alu_term = pipe * 1e3 / inst_per_upd                     # GLUPS
     achieved_gbs = alg_bytes / (avg_ms / 1e3) / 1e9
     dpi = inst_per_upd * upd_launch / (avg_ms / 1e3) / 1e12
@@ -220,7 +233,7 @@ def kernel_roofline(info, cfg, count, world, steps, k2_launches, k2_ms, ms, valu
                 "frac": achieved_gbs / hbm, "peak_kind": peak_kind}
     else:
         roof = {"bound": "alu", "achieved": dpi, "peak": pipe, "unit": "Tinst/s (fp64 DFMA/DADD/DMUL)",
-                "frac": dpi / pipe, "peak_kind": "derived: 148 SM x 64 fp64 lanes x 1.965 GHz"}
+                "frac": dpi / pipe, "peak_kind": pipe_kind}
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
