@@ -11,7 +11,8 @@
  * The ring is cut into np partitions of nx cells (N = nx*np) whose ghost
  * zones are exchanged between neighbours; here the ring is cut
  * into contiguous slabs, one per GPU rank, exchanging depth-T halos every T
- * steps (NCCL send/recv), and each GPU advances T steps per HBM pass.
+ * steps (the edge kernel's own puts into the neighbour's ghost pads over NVLink
+ * peer memory, or NCCL send/recv), and each GPU advances T steps per HBM pass.
  *
  * Conventions
  *   - All functions return int status (heat1d_status) unless stated.
@@ -163,7 +164,9 @@ HEAT1D_API int heat1d_partition(int64_t nx, int64_t np, int32_t nranks, int32_t 
 HEAT1D_API int heat1d_plan_exchange(int64_t nx, int64_t np, int32_t nranks, int32_t rank, int32_t T,
                          heat1d_exchange_plan *plan);
 
-/* Doubles of device memory a handle with these arguments allocates. */
+/* Doubles of device memory a handle with these arguments needs for its state (both
+ * ping-pong buffers of every local slab, pads for T = opts->T or, if 0, HEAT1D_T_MAX):
+ * the minimum size of opts->dev_buf.  -1 on invalid arguments. */
 HEAT1D_API int64_t heat1d_buffer_len(int64_t nx, int64_t np, const heat1d_opts *opts);
 
 /* rank 0 only: writes a 128-byte ncclUniqueId to out128 (host memory). */
