@@ -86,6 +86,8 @@ struct heat1d_s {
     unsigned long long *win_absmax = nullptr;
     int64_t win_absmax_n = 0;
     int64_t stream_windows = 0;  // windows of the last heat1d_solve_host (0 = plain sequence)
+    int64_t window_cells = 0;    // > 0: streaming handle (opts.window_cells): only solve_host
+    int64_t buf_len = 0;         // doubles per ping-pong buffer of slab 0 (as allocated)
     // transport P2P (several slabs): exchange-index words of this handle's slabs, the
     // neighbour ranks' allocations mapped over CUDA IPC, and the next exchange index
     int transport = HEAT1D_TRANSPORT_NCCL;
@@ -690,6 +692,7 @@ int64_t heat1d_buffer_len(int64_t nx, int64_t np, const heat1d_opts *o) {
     const int rank = o->virtual_slabs > 1 ? -1 : o->rank;
     const int T = o->T > 0 ? o->T : HEAT1D_T_MAX;  // auto T never exceeds the maximum
     const int64_t pad = pad_for(T);
+    if (o->window_cells > 0) return 2 * 2 * round_up(o->window_cells + 2 * pad, 32);  // 2 slots x 2 buffers
     int64_t total = 0, f, c;
     for (int g = 0; g < G; ++g) {
         if (rank >= 0 && g != rank) continue;
@@ -740,6 +743,9 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
         return set_error(nullptr, HEAT1D_EUNSUPPORTED, "virtual_slabs > 1 needs nranks == 1");
     if (o.transport != HEAT1D_TRANSPORT_NCCL && o.transport != HEAT1D_TRANSPORT_P2P)
         return set_error(nullptr, HEAT1D_EINVAL, "bad transport");
+    if (o.window_cells < 0) return set_error(nullptr, HEAT1D_EINVAL, "window_cells must be >= 0");
+    if (o.window_cells > 0 && (o.nranks > 1 || o.virtual_slabs > 1 || o.kernel != HEAT1D_KERNEL_AUTO))
+        return set_error(nullptr, HEAT1D_EUNSUPPORTED, "window_cells (streaming) needs one slab on one rank");
     if (o.T < 0 || o.T > HEAT1D_T_MAX) return set_error(nullptr, HEAT1D_EINVAL, "T must be in 0..%d", HEAT1D_T_MAX);
     const int G = o.virtual_slabs > 1 ? o.virtual_slabs : o.nranks;
     if (o.kernel == HEAT1D_KERNEL_NAIVE && G > 1)
@@ -774,6 +780,7 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     // connections lazily (cudaMalloc/IPC, illegal under capture), and a pass there is long
     // (C4 at G=8: ~1.3 ms) next to its ~3 launches.
     h->use_graphs = o.use_graphs != 0 && o.nranks == 1 && o.transport != HEAT1D_TRANSPORT_P2P;
+    h->window_cells = o.window_cells;
     h->transport = o.transport;  // (P2P pass arguments carry exchange indices: never replayed)
     h->ops = (o.mode == HEAT1D_MODE_FAST || is_pow2(r) || r == 0.0) ? 3 : 4;
     // r == 0: fma(0, t, b) == b + 0*t == b for finite t (identity either way)
@@ -823,7 +830,7 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     // K6 across ranks (one slab per rank): every rank must agree, decided after NCCL init
     bool res_multi_local = false;
     const bool res_ok = ((G == 1) || (o.nranks > 1 && o.virtual_slabs == 1)) && o.kernel == HEAT1D_KERNEL_AUTO &&
-                        o.resident != 0;
+                        o.resident != 0 && o.window_cells == 0;
     if (res_ok) {
         int64_t f0 = 0, n0 = h->N;
         if (G > 1) partition(nx, np, G, o.rank, &f0, &n0);
@@ -868,7 +875,8 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
         const int idx = (ns > 1) ? g : o.rank;
         partition(nx, np, G, idx, &s.first, &s.count);
         h->slabs.push_back(s);
-        total += 2 * round_up(s.count + 2 * h->pad, 32);
+        total += o.window_cells > 0 ? 2 * 2 * round_up(o.window_cells + 2 * h->pad, 32)
+                                    : 2 * round_up(s.count + 2 * h->pad, 32);
     }
     h->first = h->slabs.front().first;
     h->count = 0;
@@ -892,7 +900,9 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     }
     double *p = static_cast<double *>(h->alloc);
     for (auto &s : h->slabs) {
-        const int64_t len = round_up(s.count + 2 * h->pad, 32);
+        const int64_t len = o.window_cells > 0 ? 2 * round_up(o.window_cells + 2 * h->pad, 32)
+                                               : round_up(s.count + 2 * h->pad, 32);
+        h->buf_len = len;
         s.buf[0] = p;
         s.buf[1] = p + len;
         p += 2 * len;
@@ -1050,6 +1060,8 @@ static int after_initial(heat1d_t h) {
 int heat1d_set_initial(heat1d_t h, const double *u0, int64_t count) {
     int rc = guard(h);
     if (rc) return rc;
+    if (h->window_cells)
+        return set_error(h, HEAT1D_EUNSUPPORTED, "streaming handle (window_cells): use heat1d_solve_host");
     if (!u0) return set_error(h, HEAT1D_EINVAL, "u0 is NULL");
     if (count != h->count)
         return set_error(h, HEAT1D_EINVAL, "count %lld != local slab %lld", (long long)count, (long long)h->count);
@@ -1064,6 +1076,8 @@ int heat1d_set_initial(heat1d_t h, const double *u0, int64_t count) {
 int heat1d_init_uniform(heat1d_t h, uint64_t seed, double lo, double hi) {
     int rc = guard(h);
     if (rc) return rc;
+    if (h->window_cells)
+        return set_error(h, HEAT1D_EUNSUPPORTED, "streaming handle (window_cells): use heat1d_solve_host");
     if (!std::isfinite(lo) || !std::isfinite(hi)) return set_error(h, HEAT1D_EINVAL, "lo/hi not finite");
     for (const Slab &s : h->slabs) {
         CK(heat1d::launch_init_uniform(cell0(h, s, h->cur), s.count, s.first, seed, lo, hi, h->stream));
@@ -1075,6 +1089,8 @@ int heat1d_init_uniform(heat1d_t h, uint64_t seed, double lo, double hi) {
 int heat1d_run(heat1d_t h, int64_t nt) {
     int rc = guard(h);
     if (rc) return rc;
+    if (h->window_cells)
+        return set_error(h, HEAT1D_EUNSUPPORTED, "streaming handle (window_cells): use heat1d_solve_host");
     if (!h->initialized) return set_error(h, HEAT1D_ESTATE, "run before set_initial");
     if (nt < 0) nt = h->nt_default;
     if (nt == 0) return HEAT1D_OK;
@@ -1098,6 +1114,8 @@ int heat1d_run(heat1d_t h, int64_t nt) {
 int heat1d_get(heat1d_t h, double *out, int64_t count) {
     int rc = guard(h);
     if (rc) return rc;
+    if (h->window_cells)
+        return set_error(h, HEAT1D_EUNSUPPORTED, "streaming handle (window_cells): use heat1d_solve_host");
     if (!out) return set_error(h, HEAT1D_EINVAL, "out is NULL");
     if (!h->initialized) return set_error(h, HEAT1D_ESTATE, "get before set_initial");
     if (count != h->count)
@@ -1177,8 +1195,7 @@ bool fast_range_ok(heat1d_t h, unsigned long long bits) {
 bool stream_plan(heat1d_t h, int64_t nt, int64_t *C, int64_t *L, int64_t *half) {
     if (h->multi() || h->resident || h->kernel == HEAT1D_KERNEL_NAIVE || nt < 1) return false;
     const int64_t n = h->slabs[0].count;
-    const int64_t cap = round_up(n + 2 * h->pad, 32);  // doubles per ring buffer
-    *half = cap / 2 / 32 * 32;
+    *half = h->buf_len / 2 / 32 * 32;  // two window slots per ping-pong buffer
     const int64_t lw_max = *half - 2 * h->pad;
     const int64_t lmax = lw_max - 2 * nt;
     if (lmax < 16 * nt || lmax < 4096) return false;
@@ -1201,6 +1218,9 @@ int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, d
     if (nt < 0) nt = h->nt_default;
     int64_t C = 0, L = 0, half = 0;
     if (!stream_plan(h, nt, &C, &L, &half)) {  // the plain sequence
+        if (h->window_cells)
+            return set_error(h, HEAT1D_EUNSUPPORTED, "window of %lld cells too small for nt=%lld (needs >= 18 nt)",
+                             (long long)h->window_cells, (long long)nt);
         rc = heat1d_set_initial(h, u0, count);
         if (!rc) rc = heat1d_run(h, nt);
         if (!rc) rc = heat1d_get(h, out, count);

@@ -55,6 +55,7 @@ class Opts(ctypes.Structure):
         ("comm_stream", ctypes.c_void_p),
         ("transport", ctypes.c_int32),
         ("dev_buf", ctypes.c_void_p),
+        ("window_cells", ctypes.c_int64),
     ]
 
 
@@ -226,7 +227,7 @@ class Heat1D:
                  rank: int = 0, nranks: int = 1, nccl_id: Optional[bytes] = None, virtual_slabs: int = 1,
                  kernel: str = "auto", device: int = -1, stream=None, comm_stream=None,
                  blocking: bool = True, use_graphs: bool = True, resident: Optional[bool] = None,
-                 transport: str = "p2p", dev_buf=None):
+                 transport: str = "p2p", dev_buf=None, window_cells: int = 0):
         self._lib = load()
         o = default_opts()
         o.device = device
@@ -247,6 +248,7 @@ class Heat1D:
         o.stream = _stream_ptr(stream)
         o.comm_stream = _stream_ptr(comm_stream)
         o.transport = {"nccl": 0, "p2p": 1}[transport]
+        o.window_cells = window_cells
         self._dev_buf = dev_buf  # caller-owned state memory (torch tensor): kept alive with the handle
         if dev_buf is not None:
             ptr, n, _ = _data_ptr(dev_buf)

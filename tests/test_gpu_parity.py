@@ -741,3 +741,47 @@ def test_nan_poisoned_pads(h1, monkeypatch, transport):
         got = gpu_run(h1, u0, nx, np_, nt, 0.4, T=T, virtual_slabs=G, transport=transport)
         assert np.all(np.isfinite(got))
         assert_bitwise(got, want, "poisoned pads %s T=%d" % (transport, T))
+
+
+def test_streaming_handle_small_windows(h1):
+    """opts.window_cells: the device holds only two light-cone windows (rings larger than
+    HBM); heat1d_solve_host streams the ring through them -- bitwise = oracle, ragged last
+    window, the wrap; run/set_initial/get are refused; a window too small for nt is refused."""
+    N, nt, W = (1 << 22) + 5, 200, 1 << 18
+    u0 = synth.uniform(64, 0, N, -1.0, 1.0)
+    want = oracle.run(u0, 0.4, nt)
+    o = h1.default_opts()
+    o.window_cells = W
+    assert h1.buffer_len(N, 1, o) < N // 2          # vs 2 N + pads for the device-resident ring
+    with h1.Heat1D(N, 1, nt, 0.4, 1.0, 1.0, window_cells=W) as h:
+        assert_bitwise(h.solve_host(u0, nt), want, "streaming windows")
+        assert h.info()["stream_windows"] >= N // W
+        for call in (lambda: h.set_initial(u0), lambda: h.run(1), lambda: h.get()):
+            with pytest.raises(h1.Heat1DError) as ei:
+                call()
+            assert ei.value.status == 7
+        with pytest.raises(h1.Heat1DError) as ei:
+            h.solve_host(u0, W // 4)                      # nt too deep for the window
+        assert ei.value.status == 7
+    with h1.Heat1D(N, 1, nt, 0.5, 1.0, 1.0, window_cells=W, mode="fast") as h:
+        got = h.solve_host(u0, nt)
+    assert np.max(np.abs(got - oracle.run(u0, 0.5, nt))) <= fast_bound(u0, nt)
+
+
+def test_streaming_c4_ring_through_small_device_footprint(h1):
+    """The C4 ring (2^31 cells, 16 GiB per state) streamed through 2^27-cell windows
+    (~4 GiB of device memory) equals the device-resident solve bitwise, all cells."""
+    import torch
+    N, nt = C4.N, 100
+    u0 = torch.empty(N, dtype=torch.float64).pin_memory()
+    with h1.Heat1D(C4.nx, C4.np, nt, C4.k, C4.dt, C4.dx) as h:
+        h.init_uniform(C4.seed, C4.lo, C4.hi)
+        h.get(u0)
+        h.run(nt)
+        ref = torch.empty(N, dtype=torch.float64).pin_memory()
+        h.get(ref)
+    out = torch.empty(N, dtype=torch.float64).pin_memory()
+    with h1.Heat1D(C4.nx, C4.np, nt, C4.k, C4.dt, C4.dx, window_cells=1 << 27) as h:
+        h.solve_host(u0, nt, out)
+        assert h.info()["stream_windows"] >= 16
+    assert torch.equal(out, ref)
