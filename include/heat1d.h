@@ -233,7 +233,9 @@ HEAT1D_API int heat1d_profile(heat1d_t h, int64_t *launches, double *ms);
 /* Compute stream of the handle as a cudaStream_t (for the caller's events). */
 HEAT1D_API void *heat1d_stream(heat1d_t h);
 
-/* NULL-safe; frees library-owned memory, streams, events and the NCCL comm. */
+/* NULL-safe; frees library-owned memory, streams, events and the NCCL comm.  With
+ * peer-memory transports (nranks > 1) it is collective: it waits until every rank's
+ * streams are idle before unmapping or freeing anything a neighbour writes into. */
 HEAT1D_API int heat1d_destroy(heat1d_t h);
 
 /* Message for the last failing call on h ("" if none). */

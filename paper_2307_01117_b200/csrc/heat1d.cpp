@@ -1344,6 +1344,21 @@ int heat1d_destroy(heat1d_t h) {
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->comm) cudaStreamSynchronize(h->comm);
+    const bool peers = h->peer_open[0] || h->peer_open[1] || h->peer_open[2] || h->peer_open[3] ||
+                       h->mbox_ipc_left || h->mbox_ipc_right;
+    if (h->nccl && peers && !h->poisoned) {
+        // collective: a neighbour's last edge kernel may still be putting into this rank's
+        // pads (it writes ahead of any wait of ours), so nobody unmaps or frees until every
+        // rank's streams are idle
+        int *d = nullptr;
+        if (cudaMalloc(&d, sizeof(int)) == cudaSuccess) {
+            cudaMemsetAsync(d, 0, sizeof(int), h->comm);
+            if (ncclAllReduce(d, d, 1, ncclInt32, ncclSum, h->nccl, h->comm) == ncclSuccess)
+                cudaStreamSynchronize(h->comm);
+            cudaFree(d);
+        }
+        cudaGetLastError();
+    }
     if (h->nccl) ncclCommDestroy(h->nccl);
     for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
