@@ -156,10 +156,38 @@ __device__ __forceinline__ void regs_to_row(const double (&u)[V], double *row, i
     __syncwarp();
 }
 
+// Sync mode 3 ("the data is the flag"): an edge slot holds HEAT1D_EMPTY -- a signalling
+// NaN, which no fp64 arithmetic result can be (arithmetic returns quiet NaNs), and every
+// published edge value is an arithmetic result -- until its producer writes it; the
+// consumer polls the values themselves (one L2 round trip instead of release, poll and
+// two acquires), takes them and writes EMPTY back.  A fence before each publish orders
+// those resets before the data that lets the producer reuse the slot two periods later
+// (PTX fence-fence synchronisation through the observed values).
+constexpr unsigned long long HEAT1D_EMPTY = 0x7ff0dead00000001ull;
+
+__device__ __forceinline__ void st_relaxed_u64(double *p, double v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const double *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // edges: [Ns][2 parities][2 sides][T]; publish this span's period-p edges
+// (DF: data-as-flag protocol, sync mode 3, compiled into its own kernel instantiation)
+template <bool DF = false>
 __device__ __forceinline__ void publish(const Span &s, int T, unsigned p, double *edges, unsigned *flags,
                                         int lane) {
     double *E = edges + ((size_t)s.id * 4 + (p & 1) * 2) * T;
+    if constexpr (DF) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");  // earlier slot resets before this data
+        for (int i = lane; i < T; i += 32) {
+            st_relaxed_u64(E + i, s.row[T + i]);
+            st_relaxed_u64(E + T + i, s.row[s.own + i]);
+        }
+        return;
+    }
     for (int i = lane; i < T; i += 32) {
         E[i] = s.row[T + i];          // side 0: first T owned cells
         E[T + i] = s.row[s.own + i];  // side 1: last T owned cells
@@ -200,7 +228,32 @@ __device__ __forceinline__ void mbox_publish(const Span &s, int Ns, int T, unsig
 // on, the slab's outer halos come from the neighbour ranks (exchange index g)
 // initial: the exchange of the initial state (only the remote sides; the local halos
 // were loaded from the slab).
-__device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, const double *edges,
+// Data-as-flag halo refresh, kept out of line: inlined into the period loop its 64-bit
+// polls and pointers raised the matched kernels from 115 to 154 registers (and -25 %).
+__device__ __noinline__ void refresh_df(double *row, int own, int T, double *LE, double *RE, int lane) {
+    for (int i0 = 0; i0 < T; i0 += 32) {
+        const int i = i0 + lane;
+        unsigned long long l = 0, rr = 0;
+        bool ok;
+        do {
+            if (i < T) {
+                l = ld_relaxed_u64(LE + i);
+                rr = ld_relaxed_u64(RE + i);
+            }
+            ok = i >= T || (l != HEAT1D_EMPTY && rr != HEAT1D_EMPTY);
+        } while (!__all_sync(0xffffffffu, ok));
+        if (i < T) {
+            row[i] = __longlong_as_double((long long)l);
+            row[own + T + i] = __longlong_as_double((long long)rr);
+            st_relaxed_u64(LE + i, __longlong_as_double((long long)HEAT1D_EMPTY));
+            st_relaxed_u64(RE + i, __longlong_as_double((long long)HEAT1D_EMPTY));
+        }
+    }
+    __syncwarp();
+}
+
+template <bool DF = false>
+__device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, double *edges,
                                         const unsigned *flags, int lane, int sync, int Ns, const MboxArgs &mb,
                                         unsigned g, bool initial = false) {
     const bool lrem = mb.on && s.id == 0, rrem = mb.on && s.id == Ns - 1;
@@ -223,6 +276,11 @@ __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, const 
             if (doR) s.row[s.own + T + i] = __ldcg(RE + i);
         }
         __syncwarp();
+        return;
+    }
+    if constexpr (DF) {
+        refresh_df(s.row, s.own, T, edges + ((size_t)s.left * 4 + (p & 1) * 2) * T + T,
+                   edges + ((size_t)s.right * 4 + (p & 1) * 2) * T, lane);
         return;
     }
     // every lane polls (one coalesced request per poll); the vote makes the exit
@@ -257,7 +315,7 @@ __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, const 
 }  // namespace
 
 // MB: the cross-rank mailbox code is compiled in (only then: it costs ~30 registers).
-template <int V, int OPS, int SPW, bool EARLY, bool MB = false>
+template <int V, int OPS, int SPW, bool EARLY, bool MB = false, bool DF = false>
 __global__ void __launch_bounds__(256)
 k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t nt, double r,
             double rr, double *__restrict__ edges, unsigned *__restrict__ flags, int Wt, int sync, MboxArgs mb_in) {
@@ -290,9 +348,9 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
             regs_to_row<V>(ua, a.row, lane);
             done += Tp;
             if (done >= nt) break;
-            publish(a, T, p, edges, flags, lane);
+            publish<DF>(a, T, p, edges, flags, lane);
             if (mb.on) mbox_publish(a, Ns, T, mb.base + 1 + p, mb, lane);
-            refresh(a, T, p, edges, flags, lane, sync, Ns, mb, mb.base + 1 + p);
+            refresh<DF>(a, T, p, edges, flags, lane, sync, Ns, mb, mb.base + 1 + p);
             row_to_regs<V>(a.row, ua, lane);
         }
 #pragma unroll
@@ -361,11 +419,25 @@ int res_early() {
 }
 
 int res_sync() {
-    const char *e = getenv("HEAT1D_K6_SYNC");  // tuning knob (refresh's acquire pattern)
-    return e ? atoi(e) : 0;
+    // halo protocol: 3 (default) = data-as-flag; 0/1/2 = flags with the acquire after the
+    // polls / acquire polls / a fence (tuning knob HEAT1D_K6_SYNC; cross-rank and two-span
+    // kernels always use the flag protocol)
+    const char *e = getenv("HEAT1D_K6_SYNC");
+    return e ? atoi(e) : 3;
 }
 
-const void *res_fn(int ops, int spw, int rv, bool mbox = false) {
+// Data-as-flag halos for the fast (1-/2-op) kernels; the matched 3/4-op kernels keep the
+// flag protocol: compiled with data-as-flag they need ~155 instead of 115 registers and
+// lose 25 % (profiles/r01_k6_sync3.jsonl).
+bool res_df(int ops) { return res_sync() == 3 && res_early() != 0 && ops <= 2; }
+
+const void *res_fn(int ops, int spw, int rv, bool mbox = false, bool df = false) {
+    if (df && !mbox && spw == 1) {  // data-as-flag halos (early shuffles)
+#define RFD(v) (ops == 4 ? (const void *)&k6_resident<v, 4, 1, true, false, true> : ops == 3 ? (const void *)&k6_resident<v, 3, 1, true, false, true> \
+                : ops == 2 ? (const void *)&k6_resident<v, 2, 1, true, false, true> : (const void *)&k6_resident<v, 1, 1, true, false, true>)
+        return rv == 49 ? RFD(49) : rv == 33 ? RFD(33) : RFD(17);
+#undef RFD
+    }
     if (mbox) {  // SPW = 1, early shuffles, mailbox code compiled in
 #define RFM(v) (ops == 4 ? (const void *)&k6_resident<v, 4, 1, true, true> : ops == 3 ? (const void *)&k6_resident<v, 3, 1, true, true> \
                 : ops == 2 ? (const void *)&k6_resident<v, 2, 1, true, true> : (const void *)&k6_resident<v, 1, 1, true, true>)
@@ -432,7 +504,7 @@ bool res_plan(int ops, int64_t n, int T, int num_sms, ResPlan *p, bool mbox = fa
     const int64_t ns = p->wt * p->spw;
     if (n / ns < T || n / ns + (n % ns ? 1 : 0) + 2 * T > 32 * RV) return false;
     p->smem = (size_t)p->nw * p->spw * (32 * RV + 1) * sizeof(double);
-    const void *fn = res_fn(ops, p->spw, RV, mbox);
+    const void *fn = res_fn(ops, p->spw, RV, mbox, res_df(ops));
     if (res_attr(fn) != cudaSuccess) return false;
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, (int)(p->nw * 32), p->smem) != cudaSuccess)
@@ -458,6 +530,11 @@ size_t resident_scratch_bytes(int T, int num_sms) {
     return (size_t)ns * 4 * T * sizeof(double) + (size_t)ns * sizeof(unsigned) + 256;
 }
 
+__global__ void k6_fill_empty(double *edges, int64_t count) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        edges[i] = __longlong_as_double((long long)HEAT1D_EMPTY);
+}
+
 cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
                             double r, void *scratch, int num_sms, cudaStream_t st, int *warps_out,
                             const MboxArgs &mb) {
@@ -470,13 +547,19 @@ cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int 
     if (e != cudaSuccess) return e;
     int Wt = (int)p.wt;
     int sync = res_sync();
+    const bool df = res_df(ops) && p.spw == 1 && !mb.on;  // data-as-flag kernel
+    if (sync == 3 && !df) sync = 0;
+    if (df) {
+        k6_fill_empty<<<64, 256, 0, st>>>(edges, ns * 4 * (int64_t)T);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     void *args[] = {(void *)&A, (void *)&B, (void *)&n, (void *)&T, (void *)&nt, (void *)&q, (void *)&r,
                     (void *)&edges, (void *)&flags, (void *)&Wt, (void *)&sync, (void *)&mb};
     if (warps_out) *warps_out = Wt;
     if (getenv("HEAT1D_DEBUG"))
         fprintf(stderr, "[heat1d] K6 n=%lld T=%d spw=%d Wt=%d nw=%lld grid=%lld smem=%zu\n", (long long)n, T,
                 p.spw, Wt, (long long)p.nw, (long long)p.grid, p.smem);
-    return cudaLaunchCooperativeKernel(res_fn(ops, p.spw, p.rv, mb.on != 0), dim3((unsigned)p.grid), dim3((unsigned)(p.nw * 32)),
+    return cudaLaunchCooperativeKernel(res_fn(ops, p.spw, p.rv, mb.on != 0, df), dim3((unsigned)p.grid), dim3((unsigned)(p.nw * 32)),
                                        args, p.smem, st);
 }
 

@@ -146,7 +146,7 @@ def test_resident_two_span_warps(h1, monkeypatch, early):
             assert_bitwise(h.get(), oracle.run(u0, 0.5, nt), "K6 spw=2 N=%d" % N)
 
 
-@pytest.mark.parametrize("sync", ["0", "1", "2"])
+@pytest.mark.parametrize("sync", ["0", "1", "2", "3"])
 def test_resident_sync_variants(h1, monkeypatch, sync):
     """K6's three acquire patterns for the halo refresh (tuning knob HEAT1D_K6_SYNC)."""
     monkeypatch.setenv("HEAT1D_K6_SYNC", sync)
