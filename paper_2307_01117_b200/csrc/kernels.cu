@@ -631,6 +631,8 @@ PassFn lookup_pass(int V, int NW, int S, int ops, int kind) {
 
 }  // namespace
 
+bool pass_supported(const PassGeom &g, int ops) { return lookup_pass(g.V, g.NW, g.S, ops, g.kind) != nullptr; }
+
 PassGeom choose_geom(int64_t n_out, int T, int num_sms) {
     // Default (profiles/r01_sweep_kx.jsonl): CTA tiles of 4 compute
     // warps x V=49 cells/lane trading 16-deep ghosts every 16 steps (kind 4),

@@ -45,6 +45,9 @@ struct PassGeom {
     }
 };
 
+// True iff the pass kernel is instantiated for this geometry and arithmetic variant.
+bool pass_supported(const PassGeom &g, int ops);
+
 // Pick the pass-kernel configuration for (n, T).
 PassGeom choose_geom(int64_t n_out, int T, int num_sms);
 

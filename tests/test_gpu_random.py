@@ -1,0 +1,101 @@
+"""Randomised parity sweep of the CUDA path against the oracle (-m gpu).
+
+Seeded random draws over everything a caller can vary -- ring size (incl. tiny and odd),
+partitions, T, nt (tail passes), r (powers of two, general, paper-literal denominator),
+mode, kernel family (K2 kinds 0-4 via geometry, K1, K6, K6 mailbox), virtual slabs and
+both halo transports, split runs and solve_host -- each checked against the oracle:
+bitwise in matched mode, within 1e-12*max|u0|*nt in fast mode.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+GEOMS = ["", "9,4,3,4,0", "17,8,3,2,1", "33,4,3,2,2", "17,4,3,4,3", "49,4,2,2,4"]
+
+
+@pytest.fixture(scope="module")
+def h1():
+    import torch
+    from paper_2307_01117_b200 import _build
+    _build.build()
+    import paper_2307_01117_b200 as m
+    torch.cuda.set_device(0)
+    return m
+
+
+def draw(rng):
+    N = int(rng.choice([rng.integers(1, 64), rng.integers(64, 5000), rng.integers(5000, 400_000)]))
+    np_ = int(rng.choice([1, 1, 2, 3, 7]))
+    if N % np_:
+        np_ = 1
+    nx = N // np_
+    case = {
+        "N": N, "nx": nx, "np": np_,
+        "T": int(rng.choice([0, 1, 2, 5, 8, 16, 31, 64, 96])),
+        "k": float(rng.choice([0.5, 0.25, 0.4, 0.3, 0.125, 0.49])),
+        "mode": str(rng.choice(["matched", "matched", "fast"])),
+        "path": str(rng.choice(["auto", "k2", "naive", "k6", "k6mbox", "slabs_p2p", "slabs_nccl", "solve_host"])),
+        "geom": str(rng.choice(GEOMS)),
+        "runs": [int(x) for x in rng.integers(0, 40, size=int(rng.integers(1, 4)))],
+        "paper_2dx": bool(rng.random() < 0.15),
+    }
+    return case
+
+
+@pytest.mark.parametrize("seed", range(300))
+def test_random_case(h1, monkeypatch, seed):
+    rng = np.random.default_rng(1000 + seed)
+    c = draw(rng)
+    N, nt_total = c["N"], sum(c["runs"])
+    kw = {"T": c["T"], "mode": c["mode"]}
+    if c["paper_2dx"]:
+        kw["denominator"] = "paper_2dx"
+    k = c["k"] * 2 if c["paper_2dx"] else c["k"]          # same r either way
+    r = oracle.r_of(k, 1.0, 1.0, paper_2h=c["paper_2dx"])
+    path = c["path"]
+    if c["geom"] and path in ("k2", "slabs_p2p", "slabs_nccl", "solve_host"):
+        monkeypatch.setenv("HEAT1D_GEOM", c["geom"])
+    if path == "k2":
+        kw["resident"] = False
+    elif path == "naive":
+        kw = {"kernel": "naive", "mode": c["mode"]} | ({"denominator": "paper_2dx"} if c["paper_2dx"] else {})
+    elif path in ("k6", "k6mbox"):
+        kw["resident"] = True
+        if path == "k6mbox":
+            monkeypatch.setenv("HEAT1D_K6_MAILBOX", "1")
+    elif path.startswith("slabs"):
+        G = int(rng.integers(2, 6))
+        if N < 2 * G:
+            pytest.skip("ring too small for %d slabs" % G)
+        kw["virtual_slabs"] = G
+        kw["transport"] = path.split("_")[1]
+    elif path == "solve_host":
+        kw["resident"] = False
+    u0 = synth.uniform(seed, 0, N, -1.0, 1.0)
+    want = oracle.run(u0, r, nt_total)
+    try:
+        h = h1.Heat1D(c["nx"], c["np"], 0, k, 1.0, 1.0, **kw)
+    except h1.Heat1DError as e:
+        if e.status == 7:                                   # unsupported combination (e.g. K6 too large)
+            pytest.skip(str(e))
+        raise
+    with h:
+        if path == "solve_host":
+            got = h.solve_host(u0, nt_total)
+        else:
+            h.set_initial(u0)
+            for nt in c["runs"]:
+                h.run(nt)
+            got = h.get()
+    if c["mode"] == "matched":
+        if not np.array_equal(got, want):
+            bad = np.flatnonzero(got != want)
+            raise AssertionError("case %r: %d cells differ, first %d" % (c, bad.size, bad[0]))
+    else:
+        assert np.max(np.abs(got - want)) <= 1e-12 * max(1.0, float(np.max(np.abs(u0)))) * max(nt_total, 1), c
