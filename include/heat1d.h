@@ -218,7 +218,8 @@ HEAT1D_API int heat1d_get(heat1d_t h, double *out, int64_t count);
  * pinned (cudaHostAlloc / torch pin_memory) for the copies to overlap.  In fast mode
  * every window checks its own max|u0| (K5) and is recomputed with the 3-op form if
  * the scaled state could overflow (DESIGN.md c21).  Afterwards the device state is
- * consumed: call set_initial before run/get.  Errors as set_initial/run/get. */
+ * consumed: call set_initial before run/get.  u0 and out must not overlap (EINVAL).
+ * Errors as set_initial/run/get. */
 HEAT1D_API int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, double *out);
 
 HEAT1D_API int64_t heat1d_steps_done(heat1d_t h);   /* -1 if h is NULL */

@@ -1219,6 +1219,8 @@ int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, d
     if (!u0 || !out) return set_error(h, HEAT1D_EINVAL, "u0/out is NULL");
     if (count != h->count)
         return set_error(h, HEAT1D_EINVAL, "count %lld != local slab %lld", (long long)count, (long long)h->count);
+    if (out < u0 + count && u0 < out + count)  // the last windows re-read u0 after early chunks are written
+        return set_error(h, HEAT1D_EINVAL, "u0 and out must not overlap");
     if (nt < 0) nt = h->nt_default;
     int64_t C = 0, L = 0, half = 0;
     if (!stream_plan(h, nt, &C, &L, &half)) {  // the plain sequence

@@ -636,6 +636,15 @@ def test_solve_host_windows_bitwise(h1, N, nt, T):
         assert_bitwise(h.get(), want, "after solve_host")
 
 
+def test_solve_host_rejects_in_place(h1):
+    N = 300_001
+    u0 = synth.uniform(2, 0, N, -1.0, 1.0)
+    with h1.Heat1D(N, 1, 10, 0.4, 1.0, 1.0, resident=False) as h:
+        with pytest.raises(h1.Heat1DError) as ei:
+            h.solve_host(u0, 10, u0)
+        assert ei.value.status == 1
+
+
 def test_solve_host_plain_fallback(h1):
     """nt too large for windows, and the resident path: the plain three-call sequence."""
     N, nt = 10_000, 2000
