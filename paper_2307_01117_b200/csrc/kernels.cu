@@ -1,10 +1,17 @@
 // kernels.cu -- sm_100a kernels of libheat1d.
 //
-//   K2 k2_pass      T fused Jacobi steps of Eq. 2 per HBM pass (the hot kernel)
+//   K2 k2p_pass     T fused Jacobi steps of Eq. 2 per HBM pass (the hot kernel): TMA
+//                   producer warp, register-resident warp spans, kinds 2-4 (kind 4 =
+//                   default: 16-deep ghost exchange between the warps of a CTA);
+//                   k2_pass / k2w_pass are the earlier kinds 0 / 1, kept selectable
 //   K1 k1_naive     one step per launch, modular indexing (T = 1 baseline)
 //   K3 k3_edges     the two T-wide edge strips of a slab once its ghosts arrived
+//   K3p k3_edges_put  K3 fused with the halo put into the neighbours' pads (P2P
+//                   transport), with k_push_edges for the start of a run
 //   K4 k4_wrap_fill periodic self-halo of a single-slab ring
+//   K5 k5_absmax    max |u| of an initial state (fast mode's scaled-state range check)
 //   K0 k0_uniform   splitmix64 initial condition (same counter generator as synth/)
+//   (K6, the whole-solve resident kernel, is resident.cu)
 //
 // Eq. 2 on the periodic ring, segmented with
 // ghost zones.  The arithmetic is stencil.cuh; DESIGN.md §6
