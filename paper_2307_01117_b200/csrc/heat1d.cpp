@@ -361,6 +361,10 @@ int run_passes(heat1d_t h, int64_t nt) {
             // B[T, n-T), K3 writes B[0,T) and B[n-T, n): disjoint; both read A.
             CK(cudaEventRecord(h->ev_ready, h->stream));
             CK(cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
+            if (const char *dl = getenv("HEAT1D_COMM_DELAY_US")) {  // fault injection (tests)
+                CK(heat1d::launch_delay((unsigned)atoi(dl), h->comm));
+                h->launches++;
+            }
             int rc = HEAT1D_OK;
             if (h->transport == HEAT1D_TRANSPORT_P2P) {
                 // K3p: wait for the ghosts of index xg, update the strips, put them straight
@@ -824,8 +828,12 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     if (o.kernel == HEAT1D_KERNEL_NAIVE) T = 1;
     if (T > mslab) T = (int)mslab;  // a slab must hold its own halo
     if (o.transport == HEAT1D_TRANSPORT_P2P && G > 1) {
-        if (mslab < 2) return set_error(nullptr, HEAT1D_EINVAL, "transport p2p needs slabs of >= 2 cells");
-        if (T > mslab / 2) T = (int)(mslab / 2);  // K3p's two strips must not overlap
+        if (mslab < 2) {  // 1-cell slabs: K3p's two strips would overlap
+            o.transport = h->transport = HEAT1D_TRANSPORT_NCCL;
+            h->use_graphs = o.use_graphs != 0 && o.nranks == 1;
+        }
+        else if (T > mslab / 2)
+            T = (int)(mslab / 2);  // K3p's two strips must not overlap
     }
     // K6 across ranks (one slab per rank): every rank must agree, decided after NCCL init
     bool res_multi_local = false;

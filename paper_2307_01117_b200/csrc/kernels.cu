@@ -860,6 +860,18 @@ cudaError_t launch_push_edges(const double *A, int64_t n, int T, unsigned g, dou
     return cudaGetLastError();
 }
 
+// Fault injection (tests): occupy the comm stream for `us` microseconds before the halo
+// exchange of a pass (HEAT1D_COMM_DELAY_US); results must not change.
+__global__ void k_delay(unsigned us) {
+    const unsigned long long t0 = globaltimer_ns();
+    while (globaltimer_ns() - t0 < 1000ull * us) __nanosleep(1000);
+}
+
+cudaError_t launch_delay(unsigned us, cudaStream_t st) {
+    k_delay<<<1, 32, 0, st>>>(us);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ K4
 __global__ void k4_wrap_fill(double *A, int64_t n, int64_t pad) {
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < pad; j += (int64_t)gridDim.x * blockDim.x) {

@@ -79,6 +79,9 @@ cudaError_t launch_edges_put(int ops, const double *A, double *B, int64_t n, int
 cudaError_t launch_push_edges(const double *A, int64_t n, int T, unsigned g, double *put_left, double *put_right,
                               unsigned *flag_left, unsigned *flag_right, cudaStream_t st);
 
+// Test-only fault injection: a kernel that spins `us` microseconds on `st`.
+cudaError_t launch_delay(unsigned us, cudaStream_t st);
+
 // K4: fill `pad` ghost cells on each side of a single-slab ring, modularly.
 cudaError_t launch_wrap_fill(double *A, int64_t n, int64_t pad, cudaStream_t st);
 

@@ -794,3 +794,41 @@ def test_streaming_c4_ring_through_small_device_footprint(h1):
         h.solve_host(u0, nt, out)
         assert h.info()["stream_windows"] >= 16
     assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_comm_stream_delay_injection(h1, monkeypatch, transport):
+    """a 200 us spin on the comm stream before every halo exchange
+    (HEAT1D_COMM_DELAY_US) only delays the edge kernels -- results stay bitwise exact."""
+    monkeypatch.setenv("HEAT1D_COMM_DELAY_US", "200")
+    nx, np_, G, T, nt = 40_009, 4, 4, 16, 3 * 16 + 5
+    u0 = synth.uniform(4242, 0, nx * np_, -1.0, 1.0)
+    got = gpu_run(h1, u0, nx, np_, nt, 0.4, T=T, virtual_slabs=G, transport=transport)
+    assert_bitwise(got, oracle.run(u0, 0.4, nt), "delayed comm stream (%s)" % transport)
+
+
+@pytest.mark.parametrize("N", [1, 4, 10, 1000])
+@pytest.mark.parametrize("nt", [0, 1, 100])
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_spec_acceptance_grid(h1, N, nt, G):
+    """SPEC.md:468-478 acceptance criterion 1 on this build: the GPU result equals the
+    sequential oracle for N in {1,4,10,1000} x steps {0,1,100} x partitions {1,2,4,8}
+    (partitions = slabs exchanging halos; rings with fewer cells than slabs are rejected)."""
+    u0 = synth.uniform(N * 10 + G, 0, N, 0.0, 1.0)
+    if N < G:
+        with pytest.raises(h1.Heat1DError):
+            h1.Heat1D(N, 1, nt, 0.25, 1.0, 1.0, virtual_slabs=G)
+        return
+    got = gpu_run(h1, u0, N, 1, nt, 0.25, virtual_slabs=G)
+    assert_bitwise(got, oracle.run(u0, 0.25, nt), "N=%d nt=%d G=%d" % (N, nt, G))
+
+
+def test_convergence_to_the_mean(h1):
+    """SPEC.md:126/:471 on the GPU: N = 64, 1e5 steps -> every cell within 1e-6 of the mean
+    (one resident launch), bitwise equal to the oracle."""
+    N, nt = 64, 100_000
+    u0 = synth.uniform(64, 0, N, 0.0, 1.0)
+    got = gpu_run(h1, u0, N, 1, nt, 0.25)
+    assert np.max(got) - np.min(got) < 1e-6
+    assert abs(float(np.mean(got)) - float(np.mean(u0))) < 1e-9
+    assert_bitwise(got, oracle.run(u0, 0.25, nt), "convergence")
