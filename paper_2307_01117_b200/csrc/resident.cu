@@ -186,14 +186,14 @@ __device__ __forceinline__ void publish(const Span &s, int T, unsigned p, double
             st_relaxed_u64(E + i, s.row[T + i]);
             st_relaxed_u64(E + T + i, s.row[s.own + i]);
         }
-        return;
+    } else {
+        for (int i = lane; i < T; i += 32) {
+            E[i] = s.row[T + i];          // side 0: first T owned cells
+            E[T + i] = s.row[s.own + i];  // side 1: last T owned cells
+        }
+        __syncwarp();  // orders the lanes' writes before lane 0's (cumulative) release
+        if (lane == 0) st_release(flags + s.id, p + 1);
     }
-    for (int i = lane; i < T; i += 32) {
-        E[i] = s.row[T + i];          // side 0: first T owned cells
-        E[T + i] = s.row[s.own + i];  // side 1: last T owned cells
-    }
-    __syncwarp();  // orders the lanes' writes before lane 0's (cumulative) release
-    if (lane == 0) st_release(flags + s.id, p + 1);
 }
 
 // The slab's boundary spans trade halos with the neighbour RANKS through mailboxes
@@ -316,7 +316,7 @@ __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, double
 
 // MB: the cross-rank mailbox code is compiled in (only then: it costs ~30 registers).
 template <int V, int OPS, int SPW, bool EARLY, bool MB = false, bool DF = false>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, (DF && OPS >= 3) ? 2 : 0)
 k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t nt, double r,
             double rr, double *__restrict__ edges, unsigned *__restrict__ flags, int Wt, int sync, MboxArgs mb_in) {
     const MboxArgs mb = MB ? mb_in : MboxArgs{};
@@ -426,10 +426,12 @@ int res_sync() {
     return e ? atoi(e) : 3;
 }
 
-// Data-as-flag halos for the fast (1-/2-op) kernels; the matched 3/4-op kernels keep the
-// flag protocol: compiled with data-as-flag they need ~155 instead of 115 registers and
-// lose 25 % (profiles/r01_k6_sync3.jsonl).
-bool res_df(int ops) { return res_sync() == 3 && res_early() != 0 && ops <= 2; }
+// Data-as-flag halos for every arithmetic form (the matched kernels compiled with a
+// 2-blocks/SM register target: left alone ptxas gave them ~155 registers and -25 %;
+// profiles/r01_k6_sync3.jsonl).
+// (V = 17 spans -- periods T <= 32 -- keep the flag protocol: their data-as-flag build lowers
+// the co-resident CTAs per SM and no longer fits the largest on-chip rings.)
+bool res_df(int rv) { return res_sync() == 3 && res_early() != 0 && rv >= 33; }
 
 const void *res_fn(int ops, int spw, int rv, bool mbox = false, bool df = false) {
     if (df && !mbox && spw == 1) {  // data-as-flag halos (early shuffles)
@@ -504,11 +506,14 @@ bool res_plan(int ops, int64_t n, int T, int num_sms, ResPlan *p, bool mbox = fa
     const int64_t ns = p->wt * p->spw;
     if (n / ns < T || n / ns + (n % ns ? 1 : 0) + 2 * T > 32 * RV) return false;
     p->smem = (size_t)p->nw * p->spw * (32 * RV + 1) * sizeof(double);
-    const void *fn = res_fn(ops, p->spw, RV, mbox, res_df(ops));
+    const void *fn = res_fn(ops, p->spw, RV, mbox, res_df(RV));
     if (res_attr(fn) != cudaSuccess) return false;
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, (int)(p->nw * 32), p->smem) != cudaSuccess)
         return false;
+    if (getenv("HEAT1D_DEBUG"))
+        fprintf(stderr, "[heat1d] K6 plan n=%lld T=%d V=%d ops=%d spw=%d wt=%lld nw=%lld grid=%lld occ=%d smem=%zu\n",
+                (long long)n, T, RV, ops, p->spw, (long long)p->wt, (long long)p->nw, (long long)p->grid, occ, p->smem);
     return (int64_t)occ * num_sms >= p->grid;  // cooperative launch: all CTAs co-resident
 }
 
@@ -547,7 +552,7 @@ cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int 
     if (e != cudaSuccess) return e;
     int Wt = (int)p.wt;
     int sync = res_sync();
-    const bool df = res_df(ops) && p.spw == 1 && !mb.on;  // data-as-flag kernel
+    const bool df = res_df(p.rv) && p.spw == 1 && !mb.on;  // data-as-flag kernel
     if (sync == 3 && !df) sync = 0;
     if (df) {
         k6_fill_empty<<<64, 256, 0, st>>>(edges, ns * 4 * (int64_t)T);
