@@ -19,6 +19,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "kernels.h"
 #include "stencil.cuh"
@@ -457,19 +459,16 @@ const void *res_fn(int ops, int spw, int rv, bool mbox = false, bool df = false)
 #undef RF
 }
 
-cudaError_t res_attr(const void *fn) {
-    static const void *done[32] = {nullptr};
+cudaError_t res_attr(const void *fn) {  // raise the dynamic shared-memory limit once per kernel
+    static std::mutex mu;
+    static std::vector<const void *> done;
+    std::lock_guard<std::mutex> lk(mu);
     for (const void *d : done)
         if (d == fn) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         2 * 16 * (32 * 17 + 1) * 8);  // >= 8 warps x (32*33+1) too
-    if (e != cudaSuccess) return e;
-    for (auto &d : done)
-        if (!d) {
-            d = fn;
-            break;
-        }
-    return cudaSuccess;
+                                         2 * 16 * (32 * 17 + 1) * 8);  // >= 8 warps x (32*49+1) too
+    if (e == cudaSuccess) done.push_back(fn);
+    return e;
 }
 
 // Split the ring into Ns = spw*Wt equal spans (each owning >= T cells, span
