@@ -213,14 +213,25 @@ HEAT1D_API int heat1d_get(heat1d_t h, double *out, int64_t count);
  * solved on its own light-cone window [chunk - nt, chunk + nt) (indices mod N); the
  * H2D copy of window c+1 and the D2H copy of chunk c-1 run on their own streams while
  * window c computes, so a solve costs ~max(transfers, compute) instead of their sum.
- * Used for one slab on one rank when the chunks are >= 16 nt cells (redundant work
- * <= 2nt/chunk); otherwise it IS the plain three-call sequence.  u0/out should be
+ * Used for one slab per rank when the chunks are >= 16 nt cells (redundant work
+ * <= 2nt/chunk); with nranks > 1 the ranks first trade nt-deep halos once (NCCL) and then
+ * stream independently (collective; every rank takes the same branch); otherwise it IS
+ * the plain three-call sequence.  u0/out should be
  * pinned (cudaHostAlloc / torch pin_memory) for the copies to overlap.  In fast mode
  * every window checks its own max|u0| (K5) and is recomputed with the 3-op form if
  * the scaled state could overflow (DESIGN.md c21).  Afterwards the device state is
  * consumed: call set_initial before run/get.  u0 and out must not overlap (EINVAL).
  * Errors as set_initial/run/get. */
 HEAT1D_API int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, double *out);
+
+/* heat1d_solve_host for ONE slab whose neighbour cells the caller supplies: left = the nt
+ * cells preceding the slab (left[nt-1] next to u0[0]), right = the nt cells following it
+ * (host or device pointers).  The result depends on nothing else (the light cone of nt
+ * steps), so a caller that decomposes a ring itself needs no further communication.
+ * With nranks > 1 heat1d_solve_host does exactly this after one NCCL exchange of the
+ * nt-deep halos (collective).  EUNSUPPORTED if the slab is too small for the windows. */
+HEAT1D_API int heat1d_solve_host_halo(heat1d_t h, const double *u0, const double *left, const double *right,
+                                      int64_t count, int64_t nt, double *out);
 
 HEAT1D_API int64_t heat1d_steps_done(heat1d_t h);   /* -1 if h is NULL */
 HEAT1D_API int heat1d_info(heat1d_t h, heat1d_info_t *info);

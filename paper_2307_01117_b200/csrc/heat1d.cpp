@@ -1145,13 +1145,28 @@ int heat1d_get(heat1d_t h, double *out, int64_t count) {
 namespace {
 
 // Copy ring cells [a, a+len) (indices mod n, at most one wrap per side) host -> device.
-int copy_window_in(heat1d_t h, double *dst, const double *u0, int64_t n, int64_t a, int64_t len) {
+// Copy slab cells [a, a+len) to dst, a >= -H and a+len <= n+H: cells < 0 come from `left`
+// (the H cells preceding the slab, left[H-1] next to cell 0), cells >= n from `right` (the H
+// cells following it); host or device pointers.  For one slab that is the whole ring,
+// left = u0 + n - H and right = u0 (the periodic wrap).
+int copy_window_in(heat1d_t h, double *dst, const double *u0, const double *left, const double *right, int64_t H,
+                   int64_t n, int64_t a, int64_t len) {
     int64_t done = 0;
     while (done < len) {
-        int64_t g = (a + done) % n;
-        if (g < 0) g += n;
-        const int64_t run = std::min(len - done, n - g);
-        CK(cudaMemcpyAsync(dst + done, u0 + g, (size_t)run * 8, cudaMemcpyDefault, h->st_h2d));
+        const int64_t g = a + done;
+        const double *src;
+        int64_t run;
+        if (g < 0) {
+            src = left + (H + g);
+            run = std::min(len - done, -g);
+        } else if (g < n) {
+            src = u0 + g;
+            run = std::min(len - done, n - g);
+        } else {
+            src = right + (g - n);
+            run = len - done;
+        }
+        CK(cudaMemcpyAsync(dst + done, src, (size_t)run * 8, cudaMemcpyDefault, h->st_h2d));
         done += run;
     }
     return HEAT1D_OK;
@@ -1205,7 +1220,7 @@ bool fast_range_ok(heat1d_t h, unsigned long long bits) {
 // Window plan: C chunks of L cells, windows of L + 2H cells (H = nt), two slots of two
 // ping-pong buffers carved out of the handle's two ring buffers.  false = not worth it.
 bool stream_plan(heat1d_t h, int64_t nt, int64_t *C, int64_t *L, int64_t *half) {
-    if (h->multi() || h->resident || h->kernel == HEAT1D_KERNEL_NAIVE || nt < 1) return false;
+    if (h->slabs.size() > 1 || h->resident || h->kernel == HEAT1D_KERNEL_NAIVE || nt < 1) return false;
     const int64_t n = h->slabs[0].count;
     *half = h->buf_len / 2 / 32 * 32;  // two window slots per ping-pong buffer
     const int64_t lw_max = *half - 2 * h->pad;
@@ -1219,28 +1234,11 @@ bool stream_plan(heat1d_t h, int64_t nt, int64_t *C, int64_t *L, int64_t *half) 
     return *L + 2 * nt <= lw_max;
 }
 
-}  // namespace
-
-int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, double *out) {
-    int rc = guard(h);
-    if (rc) return rc;
-    if (!u0 || !out) return set_error(h, HEAT1D_EINVAL, "u0/out is NULL");
-    if (count != h->count)
-        return set_error(h, HEAT1D_EINVAL, "count %lld != local slab %lld", (long long)count, (long long)h->count);
-    if (out < u0 + count && u0 < out + count)  // the last windows re-read u0 after early chunks are written
-        return set_error(h, HEAT1D_EINVAL, "u0 and out must not overlap");
-    if (nt < 0) nt = h->nt_default;
-    int64_t C = 0, L = 0, half = 0;
-    if (!stream_plan(h, nt, &C, &L, &half)) {  // the plain sequence
-        if (h->window_cells)
-            return set_error(h, HEAT1D_EUNSUPPORTED, "window of %lld cells too small for nt=%lld (needs >= 18 nt)",
-                             (long long)h->window_cells, (long long)nt);
-        rc = heat1d_set_initial(h, u0, count);
-        if (!rc) rc = heat1d_run(h, nt);
-        if (!rc) rc = heat1d_get(h, out, count);
-        return rc;
-    }
-    rc = ensure_stream_objects(h, C);
+// The streamed solve of this handle's single slab given its nt-deep neighbour halos
+// (stream_plan must have succeeded).
+int solve_windows(heat1d_t h, const double *u0, const double *left, const double *right, int64_t nt, double *out,
+                  int64_t C, int64_t L, int64_t half) {
+    int rc = ensure_stream_objects(h, C);
     if (rc) return rc;
     const Slab &s = h->slabs[0];
     const int64_t n = s.count;
@@ -1255,7 +1253,7 @@ int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, d
         const int sl = (int)(c & 1);
         const int64_t a = c * L, len = std::min(L, n - a), Lw = len + 2 * nt;
         if (c >= 2) CK(cudaStreamWaitEvent(h->st_h2d, h->ev_out[sl], 0));  // slot free again
-        rc = copy_window_in(h, X[sl], u0, n, a - nt, Lw);
+        rc = copy_window_in(h, X[sl], u0, left, right, nt, n, a - nt, Lw);
         if (rc) return rc;
         CK(cudaEventRecord(h->ev_in[sl], h->st_h2d));
         CK(cudaStreamWaitEvent(h->stream, h->ev_in[sl], 0));
@@ -1280,7 +1278,7 @@ int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, d
         for (int64_t c = 0; c < C; ++c) {
             if (fast_range_ok(h, bits[(size_t)c])) continue;
             const int64_t a = c * L, len = std::min(L, n - a), Lw = len + 2 * nt;
-            rc = copy_window_in(h, X[0], u0, n, a - nt, Lw);
+            rc = copy_window_in(h, X[0], u0, left, right, nt, n, a - nt, Lw);
             if (rc) return rc;
             CK(cudaEventRecord(h->ev_in[0], h->st_h2d));
             CK(cudaStreamWaitEvent(h->stream, h->ev_in[0], 0));
@@ -1294,6 +1292,80 @@ int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, d
     h->steps_done = nt;
     h->stream_windows = C;
     return HEAT1D_OK;
+}
+
+int solve_checks(heat1d_t h, const double *u0, int64_t count, double *out) {
+    if (!u0 || !out) return set_error(h, HEAT1D_EINVAL, "u0/out is NULL");
+    if (count != h->count)
+        return set_error(h, HEAT1D_EINVAL, "count %lld != local slab %lld", (long long)count, (long long)h->count);
+    if (out < u0 + count && u0 < out + count)  // the last windows re-read u0 after early chunks are written
+        return set_error(h, HEAT1D_EINVAL, "u0 and out must not overlap");
+    return HEAT1D_OK;
+}
+
+}  // namespace
+
+int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, double *out) {
+    int rc = guard(h);
+    if (rc) return rc;
+    if ((rc = solve_checks(h, u0, count, out))) return rc;
+    if (nt < 0) nt = h->nt_default;
+    int64_t C = 0, L = 0, half = 0;
+    bool plan = stream_plan(h, nt, &C, &L, &half);
+    if (h->nranks > 1) {
+        // every rank must take the same branch (the plain sequence exchanges halos every pass)
+        int *d = nullptr;
+        int v = plan ? 1 : 0;
+        CK(cudaMalloc(&d, sizeof(int)));
+        CK(cudaMemcpy(d, &v, sizeof v, cudaMemcpyHostToDevice));
+        NK(ncclAllReduce(d, d, 1, ncclInt32, ncclMin, h->nccl, h->comm));
+        CK(cudaMemcpyAsync(&v, d, sizeof v, cudaMemcpyDeviceToHost, h->comm));
+        CK(cudaStreamSynchronize(h->comm));
+        CK(cudaFree(d));
+        plan = v != 0;
+    }
+    if (!plan) {  // the plain sequence
+        if (h->window_cells)
+            return set_error(h, HEAT1D_EUNSUPPORTED, "window of %lld cells too small for nt=%lld (needs >= 18 nt)",
+                             (long long)h->window_cells, (long long)nt);
+        rc = heat1d_set_initial(h, u0, count);
+        if (!rc) rc = heat1d_run(h, nt);
+        if (!rc) rc = heat1d_get(h, out, count);
+        return rc;
+    }
+    if (h->nranks == 1)  // one slab = the whole ring: the halos are its own ends (periodic wrap)
+        return solve_windows(h, u0, u0 + (count - nt), u0, nt, out, C, L, half);
+    // several ranks: ONE exchange of nt-deep halos (the light cone of the whole solve), then
+    // every rank streams its windows with no further communication
+    double *hb = nullptr;  // [send first nt | send last nt | recv left | recv right]
+    CK(cudaMalloc(&hb, (size_t)4 * nt * sizeof(double)));
+    CK(cudaMemcpyAsync(hb, u0, (size_t)nt * 8, cudaMemcpyDefault, h->comm));
+    CK(cudaMemcpyAsync(hb + nt, u0 + (count - nt), (size_t)nt * 8, cudaMemcpyDefault, h->comm));
+    const int left = (h->rank - 1 + h->nranks) % h->nranks, right = (h->rank + 1) % h->nranks;
+    NK(ncclGroupStart());
+    NK(ncclSend(hb + nt, (size_t)nt, ncclDouble, right, h->nccl, h->comm));
+    NK(ncclSend(hb, (size_t)nt, ncclDouble, left, h->nccl, h->comm));
+    NK(ncclRecv(hb + 2 * nt, (size_t)nt, ncclDouble, left, h->nccl, h->comm));
+    NK(ncclRecv(hb + 3 * nt, (size_t)nt, ncclDouble, right, h->nccl, h->comm));
+    NK(ncclGroupEnd());
+    CK(cudaStreamSynchronize(h->comm));
+    rc = solve_windows(h, u0, hb + 2 * nt, hb + 3 * nt, nt, out, C, L, half);
+    cudaFree(hb);
+    return rc;
+}
+
+int heat1d_solve_host_halo(heat1d_t h, const double *u0, const double *left, const double *right, int64_t count,
+                           int64_t nt, double *out) {
+    int rc = guard(h);
+    if (rc) return rc;
+    if ((rc = solve_checks(h, u0, count, out))) return rc;
+    if (!left || !right) return set_error(h, HEAT1D_EINVAL, "left/right halo is NULL");
+    if (nt < 0) nt = h->nt_default;
+    int64_t C = 0, L = 0, half = 0;
+    if (!stream_plan(h, nt, &C, &L, &half))
+        return set_error(h, HEAT1D_EUNSUPPORTED, "slab of %lld cells too small for light-cone windows of nt=%lld",
+                         (long long)count, (long long)nt);
+    return solve_windows(h, u0, left, right, nt, out, C, L, half);
 }
 
 int64_t heat1d_steps_done(heat1d_t h) { return h ? h->steps_done : -1; }

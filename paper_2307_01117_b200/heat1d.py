@@ -111,6 +111,7 @@ EXPORTS = (
     "heat1d_local_range", "heat1d_set_initial", "heat1d_init_uniform", "heat1d_run",
     "heat1d_get", "heat1d_steps_done", "heat1d_info", "heat1d_set_profiling",
     "heat1d_profile", "heat1d_stream", "heat1d_destroy", "heat1d_last_error", "heat1d_solve_host",
+    "heat1d_solve_host_halo",
 )
 
 _lib = None
@@ -147,6 +148,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "heat1d_run": (ctypes.c_int, [H, i64]),
         "heat1d_get": (ctypes.c_int, [H, vp, i64]),
         "heat1d_solve_host": (ctypes.c_int, [H, vp, i64, i64, vp]),
+        "heat1d_solve_host_halo": (ctypes.c_int, [H, vp, vp, vp, i64, i64, vp]),
         "heat1d_steps_done": (i64, [H]),
         "heat1d_info": (ctypes.c_int, [H, ctypes.POINTER(Info)]),
         "heat1d_set_profiling": (ctypes.c_int, [H, ctypes.c_int]),
@@ -336,6 +338,22 @@ class Heat1D:
             raise ValueError("u0 and out must hold the local slab (%d cells)" % self.count)
         _check(self._lib.heat1d_solve_host(self._h, ctypes.c_void_p(pi), n, -1 if nt is None else nt,
                                            ctypes.c_void_p(po)), self._h)
+        return out
+
+    def solve_host_halo(self, u0, left, right, nt: Optional[int] = None, out=None):
+        """Streamed solve of this slab given the nt cells before (`left`) and after (`right`)
+        it (heat1d_solve_host_halo): no communication needed."""
+        if out is None:
+            out = np.empty(self.count, dtype=np.float64)
+        pi, n, k1 = _data_ptr(u0)
+        pl, nl, k2 = _data_ptr(left)
+        pr, nr, k3 = _data_ptr(right)
+        po, m, k4 = _data_ptr(out)
+        steps = -1 if nt is None else nt
+        if n != self.count or m != self.count or (nt is not None and (nl < nt or nr < nt)):
+            raise ValueError("u0/out must hold the slab and left/right at least nt cells")
+        _check(self._lib.heat1d_solve_host_halo(self._h, ctypes.c_void_p(pi), ctypes.c_void_p(pl),
+                                                ctypes.c_void_p(pr), n, steps, ctypes.c_void_p(po)), self._h)
         return out
 
     # -- profiling of the pass kernel (CUDA events on the compute stream)

@@ -832,3 +832,32 @@ def test_convergence_to_the_mean(h1):
     assert np.max(got) - np.min(got) < 1e-6
     assert abs(float(np.mean(got)) - float(np.mean(u0))) < 1e-9
     assert_bitwise(got, oracle.run(u0, 0.25, nt), "convergence")
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+@pytest.mark.parametrize("mode", ["matched", "fast"])
+def test_solve_host_halo_emulates_ranks(h1, G, mode):
+    """heat1d_solve_host_halo -- the per-rank half of the multi-rank heat1d_solve_host (one
+    exchange of nt-deep halos, then no communication): G slabs of a ring, each solved by its
+    own handle from its cells plus the nt cells on either side, reassemble the oracle's ring
+    bitwise (matched) / within the bound (fast)."""
+    N, nt = 3_000_017, 150
+    u0 = synth.uniform(300 + G, 0, N, -1.0, 1.0)
+    want = oracle.run(u0, 0.4, nt)
+    parts = []
+    for g in range(G):
+        first, count = h1.partition(N, 1, G, g)
+        idx = np.arange(first - nt, first + count + nt) % N
+        ext = u0[idx]
+        with h1.Heat1D(count, 1, nt, 0.4, 1.0, 1.0, resident=False, mode=mode) as h:
+            parts.append(h.solve_host_halo(ext[nt:nt + count].copy(), ext[:nt].copy(), ext[nt + count:].copy(), nt))
+            assert h.info()["stream_windows"] >= 2
+    got = np.concatenate(parts)
+    if mode == "matched":
+        assert_bitwise(got, want, "solve_host_halo G=%d" % G)
+    else:
+        assert np.max(np.abs(got - want)) <= fast_bound(u0, nt)
+    with h1.Heat1D(1000, 1, 100, 0.4, 1.0, 1.0, resident=False) as h:       # slab too small for windows
+        with pytest.raises(h1.Heat1DError) as ei:
+            h.solve_host_halo(u0[:1000].copy(), u0[:100].copy(), u0[:100].copy(), 100)
+        assert ei.value.status == 7
