@@ -1350,8 +1350,16 @@ int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, d
     NK(ncclGroupEnd());
     CK(cudaStreamSynchronize(h->comm));
     rc = solve_windows(h, u0, hb + 2 * nt, hb + 3 * nt, nt, out, C, L, half);
-    cudaFree(hb);
-    return rc;
+    if (rc) {
+        cudaFree(hb);
+        return rc;
+    }
+    // leave together: the windows occupy the slab buffers, pads included, which a neighbour's
+    // next run would start pushing edges into (P2P transport)
+    NK(ncclAllReduce(hb, hb, 1, ncclDouble, ncclSum, h->nccl, h->comm));
+    CK(cudaStreamSynchronize(h->comm));
+    CK(cudaFree(hb));
+    return HEAT1D_OK;
 }
 
 int heat1d_solve_host_halo(heat1d_t h, const double *u0, const double *left, const double *right, int64_t count,
