@@ -114,3 +114,60 @@ def test_slab_exchange_plan_gloo(world, nx, np_, T, nt, k):
     u0 = synth.uniform(31, 0, nx * np_, -1.0, 1.0)
     want = oracle.run(u0, k, nt)
     np.testing.assert_array_equal(got, want)
+
+
+def _worker_light_cone(rank, world, port, N, nt, k, seed, out_q):
+    """The host-array multi-rank solve (heat1d_solve_host, nranks > 1): ONE exchange of
+    nt-deep halos -- in the same issue order as the library's NCCL group -- then every rank
+    finishes on its own (here with the oracle's light-cone window, O3)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import paper_2307_01117_b200 as h1
+        import synth
+        first, count = h1.partition(N, 1, world, rank)
+        u = torch.from_numpy(synth.uniform(seed, first, count, -1.0, 1.0))
+        left, right = (rank - 1) % world, (rank + 1) % world
+        s_last, s_first = u[count - nt:].clone(), u[:nt].clone()
+        r_left, r_right = torch.empty(nt, dtype=torch.float64), torch.empty(nt, dtype=torch.float64)
+        reqs = [dist.isend(s_last, right), dist.isend(s_first, left), dist.irecv(r_left, left),
+                dist.irecv(r_right, right)]
+        for q in reqs:
+            q.wait()
+        w0 = np.concatenate([r_left.numpy(), u.numpy(), r_right.numpy()])
+        mine = oracle.window(w0, nt, float(k))
+        parts = [None] * world
+        dist.all_gather_object(parts, (first, mine))
+        if rank == 0:
+            out_q.put(parts)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,N,nt", [(2, 5000, 300), (3, 4099, 200)])
+def test_one_deep_halo_exchange_suffices_gloo(world, N, nt):
+    """Light cone across ranks: after one exchange of nt-deep halos no rank needs anything
+    else for the whole nt-step solve; the reassembled ring equals the oracle bitwise."""
+    import oracle
+    import synth
+    from paper_2307_01117_b200 import _build
+    _build.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker_light_cone, args=(rk, world, port, N, nt, 0.4, 77, q)) for rk in range(world)]
+    for p in procs:
+        p.start()
+    parts = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    parts.sort(key=lambda t: t[0])
+    got = np.concatenate([a for _, a in parts])
+    np.testing.assert_array_equal(got, oracle.run(synth.uniform(77, 0, N, -1.0, 1.0), 0.4, nt))
