@@ -482,7 +482,8 @@ int setup_multi_resident(heat1d_t h, bool local_fits) {
         return HEAT1D_OK;  // K2 passes + NCCL exchange
     }
     CK(cudaMalloc(&h->mbox, heat1d::MBOX_BYTES));
-    CK(cudaMemset(h->mbox, 0, heat1d::MBOX_BYTES));
+    CK(heat1d::launch_mbox_init(h->mbox, h->comm));
+    CK(cudaStreamSynchronize(h->comm));
     cudaIpcMemHandle_t mineh;
     CK(cudaIpcGetMemHandle(&mineh, h->mbox));
     char *dh = nullptr;
@@ -983,7 +984,8 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
         (!h->ops_fast || heat1d::resident_fits(h->ops_fast, h->N, h->T, h->num_sms, true))) {
         // test knob: route the single rank's wrap through its own mailbox (the multi-rank protocol)
         if (cudaMalloc(&h->mbox, heat1d::MBOX_BYTES) != cudaSuccess ||
-            cudaMemset(h->mbox, 0, heat1d::MBOX_BYTES) != cudaSuccess) {
+            heat1d::launch_mbox_init(h->mbox, h->stream) != cudaSuccess ||
+            cudaStreamSynchronize(h->stream) != cudaSuccess) {
             cudaGetLastError();
             set_error(nullptr, HEAT1D_ENOMEM, "mailbox");
             return bail(HEAT1D_ENOMEM);

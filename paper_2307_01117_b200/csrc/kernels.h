@@ -105,6 +105,9 @@ struct MboxArgs {
     int on = 0;
 };
 
+// Initialise a mailbox: data slots to the data-as-flag EMPTY pattern, flag words to 0.
+cudaError_t launch_mbox_init(double *mbox, cudaStream_t st);
+
 // K6: whole nt-step solve of a single-slab ring held in registers (resident.cu).
 int64_t resident_capacity(int T, int num_sms);
 bool resident_fits(int ops, int64_t n, int T, int num_sms, bool mbox = false);  // plan + co-residency

@@ -167,26 +167,45 @@ __device__ __forceinline__ void regs_to_row(const double (&u)[V], double *row, i
 // (PTX fence-fence synchronisation through the observed values).
 constexpr unsigned long long HEAT1D_EMPTY = 0x7ff0dead00000001ull;
 
+// SYS: system scope (mailboxes written by a peer GPU over NVLink), else GPU scope.
+template <bool SYS = false>
 __device__ __forceinline__ void st_relaxed_u64(double *p, double v) {
-    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)) : "memory");
+    if constexpr (SYS)
+        asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)) : "memory");
+    else
+        asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)) : "memory");
 }
+template <bool SYS = false>
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const double *p) {
     unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    if constexpr (SYS)
+        asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+template <bool SYS = false>
+__device__ __forceinline__ void fence_acq_rel() {
+    if constexpr (SYS)
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+    else
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+// an initial-state value that happens to be the EMPTY pattern is sent quieted (fp64
+// arithmetic on either NaN gives the same canonical NaN)
+constexpr unsigned long long HEAT1D_EMPTY_QUIET = HEAT1D_EMPTY | (1ull << 51);
 
 // edges: [Ns][2 parities][2 sides][T]; publish this span's period-p edges
 // (DF: data-as-flag protocol, sync mode 3, compiled into its own kernel instantiation)
-template <bool DF = false>
+template <bool DF = false, bool SYS = false>
 __device__ __forceinline__ void publish(const Span &s, int T, unsigned p, double *edges, unsigned *flags,
                                         int lane) {
     double *E = edges + ((size_t)s.id * 4 + (p & 1) * 2) * T;
     if constexpr (DF) {
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");  // earlier slot resets before this data
+        fence_acq_rel<SYS>();  // earlier slot resets (local and, SYS, in the mailbox) before this data
         for (int i = lane; i < T; i += 32) {
-            st_relaxed_u64(E + i, s.row[T + i]);
-            st_relaxed_u64(E + T + i, s.row[s.own + i]);
+            st_relaxed_u64<SYS>(E + i, s.row[T + i]);
+            st_relaxed_u64<SYS>(E + T + i, s.row[s.own + i]);
         }
     } else {
         for (int i = lane; i < T; i += 32) {
@@ -211,7 +230,26 @@ __device__ __forceinline__ unsigned *mbox_flag(double *mb, int side) {
     return reinterpret_cast<unsigned *>(reinterpret_cast<char *>(mb) + MBOX_FLAG_OFF) + side * 32;
 }
 
-__device__ __forceinline__ void mbox_publish(const Span &s, int Ns, int T, unsigned g, const MboxArgs &mb, int lane) {
+// DF: data-as-flag across GPUs -- the values go straight into the neighbour's mailbox
+// slot (EMPTY until written, reset by its reader), no flag; the fence orders this rank's
+// earlier resets of its own mailbox before the data that lets the neighbour reuse them.
+template <bool DF = false>
+__device__ __forceinline__ void mbox_publish(const Span &s, int Ns, int T, unsigned g, const MboxArgs &mb, int lane,
+                                             bool fenced = false) {
+    if constexpr (DF) {
+        if (!fenced) fence_acq_rel<true>();  // (publish<DF, true> just issued one)
+        auto put = [&](double *D, const double *src) {
+            for (int i = lane; i < T; i += 32) {
+                double x = src[i];
+                if ((unsigned long long)__double_as_longlong(x) == HEAT1D_EMPTY)
+                    x = __longlong_as_double((long long)HEAT1D_EMPTY_QUIET);
+                st_relaxed_u64<true>(D + i, x);
+            }
+        };
+        if (s.id == 0) put(mbox_data(mb.left, 1, g), s.row + T);
+        if (s.id == Ns - 1) put(mbox_data(mb.right, 0, g), s.row + s.own);
+        return;
+    }
     if (s.id == 0) {
         double *D = mbox_data(mb.left, 1, g);
         for (int i = lane; i < T; i += 32) D[i] = s.row[T + i];
@@ -232,33 +270,48 @@ __device__ __forceinline__ void mbox_publish(const Span &s, int Ns, int T, unsig
 // were loaded from the slab).
 // Data-as-flag halo refresh, kept out of line: inlined into the period loop its 64-bit
 // polls and pointers raised the matched kernels from 115 to 154 registers (and -25 %).
-__device__ __noinline__ void refresh_df(double *row, int own, int T, double *LE, double *RE, int lane) {
+// doL/doR false: that side's halo is already valid (the initial exchange of local sides).
+template <bool SYS>
+__device__ __noinline__ void refresh_df(double *row, int own, int T, double *LE, double *RE, bool doL, bool doR,
+                                        int lane) {
+    const unsigned long long t0 = SYS ? globaltimer_ns() : 0;
     for (int i0 = 0; i0 < T; i0 += 32) {
         const int i = i0 + lane;
         unsigned long long l = 0, rr = 0;
         bool ok;
         do {
             if (i < T) {
-                l = ld_relaxed_u64(LE + i);
-                rr = ld_relaxed_u64(RE + i);
+                if (doL) l = ld_relaxed_u64<SYS>(LE + i);
+                if (doR) rr = ld_relaxed_u64<SYS>(RE + i);
             }
-            ok = i >= T || (l != HEAT1D_EMPTY && rr != HEAT1D_EMPTY);
+            ok = i >= T || ((!doL || l != HEAT1D_EMPTY) && (!doR || rr != HEAT1D_EMPTY));
+            if (SYS && globaltimer_ns() - t0 > HEAT1D_WAIT_NS) __trap();  // a neighbour rank is gone
         } while (!__all_sync(0xffffffffu, ok));
         if (i < T) {
-            row[i] = __longlong_as_double((long long)l);
-            row[own + T + i] = __longlong_as_double((long long)rr);
-            st_relaxed_u64(LE + i, __longlong_as_double((long long)HEAT1D_EMPTY));
-            st_relaxed_u64(RE + i, __longlong_as_double((long long)HEAT1D_EMPTY));
+            if (doL) {
+                row[i] = __longlong_as_double((long long)l);
+                st_relaxed_u64<SYS>(LE + i, __longlong_as_double((long long)HEAT1D_EMPTY));
+            }
+            if (doR) {
+                row[own + T + i] = __longlong_as_double((long long)rr);
+                st_relaxed_u64<SYS>(RE + i, __longlong_as_double((long long)HEAT1D_EMPTY));
+            }
         }
     }
     __syncwarp();
 }
 
-template <bool DF = false>
+template <bool DF = false, bool SYS = false>
 __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, double *edges,
                                         const unsigned *flags, int lane, int sync, int Ns, const MboxArgs &mb,
                                         unsigned g, bool initial = false) {
     const bool lrem = mb.on && s.id == 0, rrem = mb.on && s.id == Ns - 1;
+    if constexpr (DF) {
+        double *LE = lrem ? mbox_data(mb.self, 0, g) : edges + ((size_t)s.left * 4 + (p & 1) * 2) * T + T;
+        double *RE = rrem ? mbox_data(mb.self, 1, g) : edges + ((size_t)s.right * 4 + (p & 1) * 2) * T;
+        refresh_df<SYS>(s.row, s.own, T, LE, RE, lrem || !initial, rrem || !initial, lane);
+        return;
+    }
     if (lrem || rrem) {
         const bool doL = lrem || !initial, doR = rrem || !initial;
         const unsigned *Lf = lrem ? mbox_flag(mb.self, 0) : flags + s.left;
@@ -278,11 +331,6 @@ __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, double
             if (doR) s.row[s.own + T + i] = __ldcg(RE + i);
         }
         __syncwarp();
-        return;
-    }
-    if constexpr (DF) {
-        refresh_df(s.row, s.own, T, edges + ((size_t)s.left * 4 + (p & 1) * 2) * T + T,
-                   edges + ((size_t)s.right * 4 + (p & 1) * 2) * T, lane);
         return;
     }
     // every lane polls (one coalesced request per poll); the vote makes the exit
@@ -338,8 +386,8 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
 
     if constexpr (SPW == 1) {
         if (mb.on && (a.id == 0 || a.id == Ns - 1)) {  // outer halos of the initial state: neighbour ranks
-            mbox_publish(a, Ns, T, mb.base, mb, lane);
-            refresh(a, T, 0, edges, flags, lane, sync, Ns, mb, mb.base, true);
+            mbox_publish<DF>(a, Ns, T, mb.base, mb, lane);
+            refresh<DF, MB>(a, T, 0, edges, flags, lane, sync, Ns, mb, mb.base, true);
             row_to_regs<V>(a.row, ua, lane);
         }
         int64_t done = 0;
@@ -350,9 +398,16 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
             regs_to_row<V>(ua, a.row, lane);
             done += Tp;
             if (done >= nt) break;
-            publish<DF>(a, T, p, edges, flags, lane);
-            if (mb.on) mbox_publish(a, Ns, T, mb.base + 1 + p, mb, lane);
-            refresh<DF>(a, T, p, edges, flags, lane, sync, Ns, mb, mb.base + 1 + p);
+            // system scope only for the slab's two boundary spans (their halos cross GPUs):
+            // a .sys fence in every warp every period cost more than half of C5's speed
+            if (MB && mb.on && (a.id == 0 || a.id == Ns - 1)) {
+                publish<DF, true>(a, T, p, edges, flags, lane);
+                mbox_publish<DF>(a, Ns, T, mb.base + 1 + p, mb, lane, true);
+                refresh<DF, true>(a, T, p, edges, flags, lane, sync, Ns, mb, mb.base + 1 + p);
+            } else {
+                publish<DF, false>(a, T, p, edges, flags, lane);
+                refresh<DF, false>(a, T, p, edges, flags, lane, sync, Ns, mb, mb.base + 1 + p);
+            }
             row_to_regs<V>(a.row, ua, lane);
         }
 #pragma unroll
@@ -441,6 +496,12 @@ const void *res_fn(int ops, int spw, int rv, bool mbox = false, bool df = false)
                 : ops == 2 ? (const void *)&k6_resident<v, 2, 1, true, false, true> : (const void *)&k6_resident<v, 1, 1, true, false, true>)
         return rv == 49 ? RFD(49) : rv == 33 ? RFD(33) : RFD(17);
 #undef RFD
+    }
+    if (mbox && df) {  // SPW = 1, early shuffles, mailbox + data-as-flag across GPUs
+#define RFMD(v) (ops == 4 ? (const void *)&k6_resident<v, 4, 1, true, true, true> : ops == 3 ? (const void *)&k6_resident<v, 3, 1, true, true, true> \
+                 : ops == 2 ? (const void *)&k6_resident<v, 2, 1, true, true, true> : (const void *)&k6_resident<v, 1, 1, true, true, true>)
+        return rv == 49 ? RFMD(49) : RFMD(33);
+#undef RFMD
     }
     if (mbox) {  // SPW = 1, early shuffles, mailbox code compiled in
 #define RFM(v) (ops == 4 ? (const void *)&k6_resident<v, 4, 1, true, true> : ops == 3 ? (const void *)&k6_resident<v, 3, 1, true, true> \
@@ -539,6 +600,13 @@ __global__ void k6_fill_empty(double *edges, int64_t count) {
         edges[i] = __longlong_as_double((long long)HEAT1D_EMPTY);
 }
 
+cudaError_t launch_mbox_init(double *mbox, cudaStream_t st) {  // every data slot EMPTY, flags 0
+    cudaError_t e = cudaMemsetAsync(mbox, 0, MBOX_BYTES, st);
+    if (e != cudaSuccess) return e;
+    k6_fill_empty<<<4, 128, 0, st>>>(mbox, (int64_t)(MBOX_FLAG_OFF / sizeof(double)));
+    return cudaGetLastError();
+}
+
 cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
                             double r, void *scratch, int num_sms, cudaStream_t st, int *warps_out,
                             const MboxArgs &mb) {
@@ -551,7 +619,7 @@ cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int 
     if (e != cudaSuccess) return e;
     int Wt = (int)p.wt;
     int sync = res_sync();
-    const bool df = res_df(p.rv) && p.spw == 1 && !mb.on;  // data-as-flag kernel
+    const bool df = res_df(p.rv) && p.spw == 1;  // data-as-flag kernel (local and mailbox halos)
     if (sync == 3 && !df) sync = 0;
     if (df) {
         k6_fill_empty<<<64, 256, 0, st>>>(edges, ns * 4 * (int64_t)T);
