@@ -53,17 +53,36 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     inc, lib = nccl_dirs()
     nvcc = os.environ.get("NVCC", "nvcc")
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    common = [nvcc, "-std=c++17", "-O3", *ARCH, "-lineinfo", "-Xptxas", "-v",
+              "-Xcompiler", "-fPIC,-fvisibility=hidden", "-DHEAT1D_BUILD", "-I", INCLUDE, "-I", CSRC, "-I", inc]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".%d.o" % os.getpid())
+        cmd = common + ["-c", src, "-o", obj]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        return obj, " ".join(cmd) + "\n" + res.stdout + res.stderr, res.returncode
+
+    # one nvcc per translation unit, in parallel (the pass-kernel instantiations dominate)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(sources())) as ex:
+        results = list(ex.map(compile_one, sources()))
+    log = "".join(r[1] for r in results)
     tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [nvcc, "-std=c++17", "-O3", *ARCH, "-lineinfo", "-Xptxas", "-v",
-           "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared",
-           "-DHEAT1D_BUILD", "-I", INCLUDE, "-I", CSRC, "-I", inc,
-           *sources(), "-o", tmp,
-           "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    log = res.stdout + res.stderr
+    ok = all(r[2] == 0 for r in results)
+    if ok:
+        cmd = [nvcc, *ARCH, "-shared", *[r[0] for r in results], "-o", tmp,
+               "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        log += " ".join(cmd) + "\n" + res.stdout + res.stderr
+        ok = res.returncode == 0
+    for r in results:
+        if os.path.exists(r[0]):
+            os.remove(r[0])
     with open(os.path.join(HERE, "build.log"), "w") as f:
-        f.write(" ".join(cmd) + "\n" + log)
-    if res.returncode != 0:
+        f.write(log)
+    if not ok:
         sys.stderr.write(log)
         raise RuntimeError("nvcc failed (see paper_2307_01117_b200/build.log)")
     if verbose:
