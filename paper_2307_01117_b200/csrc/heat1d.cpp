@@ -22,7 +22,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <chrono>
 #include <cstring>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -1449,9 +1451,20 @@ int heat1d_destroy(heat1d_t h) {
         int *d = nullptr;
         if (cudaMalloc(&d, sizeof(int)) == cudaSuccess) {
             cudaMemsetAsync(d, 0, sizeof(int), h->comm);
-            if (ncclAllReduce(d, d, 1, ncclInt32, ncclSum, h->nccl, h->comm) == ncclSuccess)
-                cudaStreamSynchronize(h->comm);
-            cudaFree(d);
+            if (ncclAllReduce(d, d, 1, ncclInt32, ncclSum, h->nccl, h->comm) == ncclSuccess) {
+                // a rank that never destroys (it died, or leaked its handle) must not hang the
+                // others forever: give up after 30 s and abort the communicator
+                const auto t0 = std::chrono::steady_clock::now();
+                while (cudaStreamQuery(h->comm) == cudaErrorNotReady) {
+                    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30)) {
+                        ncclCommAbort(h->nccl);
+                        h->nccl = nullptr;
+                        break;
+                    }
+                    std::this_thread::sleep_for(std::chrono::microseconds(50));
+                }
+            }
+            if (h->nccl) cudaFree(d);  // (after an abort the stream may still hold the reduce)
         }
         cudaGetLastError();
     }
