@@ -105,7 +105,7 @@ def run_once(me, ranks, nt, r, rng):
             put(L, me.cur, 1, A[T:2 * T].copy(), me.xg, rng)
             put(R, me.cur, 0, A[n:n + T].copy(), me.xg, rng)
         g = me.xg
-        wait_flags(me, g, time.time() + 20)
+        wait_flags(me, g, time.time() + 3)
         with me.lock:                     # K3p reads its window: pads must hold index g
             assert me.tag[me.cur] == [g, g], (me.g, me.cur, me.tag[me.cur], g)
             win_l = A[T - Tp:T + 2 * Tp].copy()
