@@ -112,7 +112,7 @@ typedef struct {
                                tensor): >= heat1d_buffer_len(nx, np, opts) doubles, 256-byte
                                aligned, outliving the handle; NULL = the handle cudaMallocs   */
     int64_t window_cells;   /* > 0: STREAMING handle for rings larger than device memory: the
-                               device holds only two light-cone windows of this many cells
+                               device holds only three light-cone windows of this many cells
                                (x2 ping-pong buffers); only heat1d_solve_host is available
                                (window_cells >= 18*nt); 0 (default) = the whole ring on device */
 } heat1d_opts;

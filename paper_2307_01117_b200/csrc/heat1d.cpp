@@ -84,7 +84,7 @@ struct heat1d_s {
     bool own_stream = false, own_comm = false;
     // heat1d_solve_host: copy streams, per-slot events, per-window max|u0| words
     cudaStream_t st_h2d = nullptr, st_d2h = nullptr;
-    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+    cudaEvent_t ev_in[3] = {}, ev_comp[3] = {}, ev_out[3] = {};  // per window slot
     unsigned long long *win_absmax = nullptr;
     int64_t win_absmax_n = 0;
     int64_t stream_windows = 0;  // windows of the last heat1d_solve_host (0 = plain sequence)
@@ -699,7 +699,7 @@ int64_t heat1d_buffer_len(int64_t nx, int64_t np, const heat1d_opts *o) {
     const int rank = o->virtual_slabs > 1 ? -1 : o->rank;
     const int T = o->T > 0 ? o->T : HEAT1D_T_MAX;  // auto T never exceeds the maximum
     const int64_t pad = pad_for(T);
-    if (o->window_cells > 0) return 2 * 2 * round_up(o->window_cells + 2 * pad, 32);  // 2 slots x 2 buffers
+    if (o->window_cells > 0) return 3 * 2 * round_up(o->window_cells + 2 * pad, 32);  // 3 slots x 2 buffers
     int64_t total = 0, f, c;
     for (int g = 0; g < G; ++g) {
         if (rank >= 0 && g != rank) continue;
@@ -886,7 +886,7 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
         const int idx = (ns > 1) ? g : o.rank;
         partition(nx, np, G, idx, &s.first, &s.count);
         h->slabs.push_back(s);
-        total += o.window_cells > 0 ? 2 * 2 * round_up(o.window_cells + 2 * h->pad, 32)
+        total += o.window_cells > 0 ? 3 * 2 * round_up(o.window_cells + 2 * h->pad, 32)
                                     : 2 * round_up(s.count + 2 * h->pad, 32);
     }
     h->first = h->slabs.front().first;
@@ -911,7 +911,7 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     }
     double *p = static_cast<double *>(h->alloc);
     for (auto &s : h->slabs) {
-        const int64_t len = o.window_cells > 0 ? 2 * round_up(o.window_cells + 2 * h->pad, 32)
+        const int64_t len = o.window_cells > 0 ? 3 * round_up(o.window_cells + 2 * h->pad, 32)
                                                : round_up(s.count + 2 * h->pad, 32);
         h->buf_len = len;
         s.buf[0] = p;
@@ -1198,7 +1198,7 @@ int solve_window(heat1d_t h, int ops, double *X, double *Y, int64_t Lw, int64_t 
 int ensure_stream_objects(heat1d_t h, int64_t nwin) {
     if (!h->st_h2d) CK(cudaStreamCreateWithFlags(&h->st_h2d, cudaStreamNonBlocking));
     if (!h->st_d2h) CK(cudaStreamCreateWithFlags(&h->st_d2h, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 3; ++i) {
         if (!h->ev_in[i]) CK(cudaEventCreateWithFlags(&h->ev_in[i], cudaEventDisableTiming));
         if (!h->ev_comp[i]) CK(cudaEventCreateWithFlags(&h->ev_comp[i], cudaEventDisableTiming));
         if (!h->ev_out[i]) CK(cudaEventCreateWithFlags(&h->ev_out[i], cudaEventDisableTiming));
@@ -1213,6 +1213,8 @@ int ensure_stream_objects(heat1d_t h, int64_t nwin) {
     return HEAT1D_OK;
 }
 
+constexpr int kWinSlots = 3;  // light-cone window slots per ping-pong buffer (heat1d_solve_host)
+
 bool fast_range_ok(heat1d_t h, unsigned long long bits) {
     double m;
     memcpy(&m, &bits, sizeof m);
@@ -1226,7 +1228,7 @@ bool fast_range_ok(heat1d_t h, unsigned long long bits) {
 bool stream_plan(heat1d_t h, int64_t nt, int64_t *C, int64_t *L, int64_t *half) {
     if (h->slabs.size() > 1 || h->resident || h->kernel == HEAT1D_KERNEL_NAIVE || nt < 1) return false;
     const int64_t n = h->slabs[0].count;
-    *half = h->buf_len / 2 / 32 * 32;  // two window slots per ping-pong buffer
+    *half = h->buf_len / kWinSlots / 32 * 32;  // window slots per ping-pong buffer
     const int64_t lw_max = *half - 2 * h->pad;
     const int64_t lmax = lw_max - 2 * nt;
     if (lmax < 16 * nt || lmax < 4096) return false;
@@ -1247,16 +1249,22 @@ int solve_windows(heat1d_t h, const double *u0, const double *left, const double
     const Slab &s = h->slabs[0];
     const int64_t n = s.count;
     const int ops = h->ops_fast ? h->ops_fast : h->ops;  // optimistic; checked per window below
-    double *X[2] = {s.buf[0] + h->pad, s.buf[0] + half + h->pad};
-    double *Y[2] = {s.buf[1] + h->pad, s.buf[1] + half + h->pad};
+    // three window slots: the H2D of window c+1, the compute of window c and the D2H of
+    // window c-1 each own one, so the three run fully concurrently (two slots serialise
+    // a D2H before the next H2D into the same slot)
+    double *X[kWinSlots], *Y[kWinSlots];
+    for (int k = 0; k < kWinSlots; ++k) {
+        X[k] = s.buf[0] + k * half + h->pad;
+        Y[k] = s.buf[1] + k * half + h->pad;
+    }
     h->initialized = false;  // the ring buffers now hold windows
     if (h->ops_fast) CK(cudaMemsetAsync(h->win_absmax, 0, (size_t)C * 8, h->stream));
     CK(cudaEventRecord(h->ev_comp[0], h->stream));  // memset before any K5
     CK(cudaStreamWaitEvent(h->st_h2d, h->ev_comp[0], 0));
     for (int64_t c = 0; c < C; ++c) {
-        const int sl = (int)(c & 1);
+        const int sl = (int)(c % kWinSlots);
         const int64_t a = c * L, len = std::min(L, n - a), Lw = len + 2 * nt;
-        if (c >= 2) CK(cudaStreamWaitEvent(h->st_h2d, h->ev_out[sl], 0));  // slot free again
+        if (c >= kWinSlots) CK(cudaStreamWaitEvent(h->st_h2d, h->ev_out[sl], 0));  // slot free again
         rc = copy_window_in(h, X[sl], u0, left, right, nt, n, a - nt, Lw);
         if (rc) return rc;
         CK(cudaEventRecord(h->ev_in[sl], h->st_h2d));
@@ -1485,7 +1493,7 @@ int heat1d_destroy(heat1d_t h) {
         if (h->peer_open[i]) cudaIpcCloseMemHandle(i % 2 == 0 ? h->peer_alloc[i / 2] : h->peer_flags[i / 2]);
     if (h->xflags) cudaFree(h->xflags);
     if (h->win_absmax) cudaFree(h->win_absmax);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 3; ++i) {
         if (h->ev_in[i]) cudaEventDestroy(h->ev_in[i]);
         if (h->ev_comp[i]) cudaEventDestroy(h->ev_comp[i]);
         if (h->ev_out[i]) cudaEventDestroy(h->ev_out[i]);
