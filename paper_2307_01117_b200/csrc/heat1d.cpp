@@ -998,7 +998,7 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     // this handle may run (its matched/fast form and the 3-op fallback); else the default
     if (!parse_geom_env(&h->geom) || !heat1d::pass_supported(h->geom, h->ops) ||
         (h->ops_fast && !heat1d::pass_supported(h->geom, h->ops_fast)) || !heat1d::pass_supported(h->geom, 3))
-        h->geom = heat1d::choose_geom(h->slabs[0].count, h->T, h->num_sms);
+        h->geom = heat1d::choose_geom(h->slabs[0].count, h->T, h->num_sms, h->ops_fast ? h->ops_fast : h->ops);
     if (h->ops_fast && cudaMalloc(&h->absmax, sizeof(unsigned long long)) != cudaSuccess) {
         cudaGetLastError();
         set_error(nullptr, HEAT1D_ENOMEM, "absmax word");

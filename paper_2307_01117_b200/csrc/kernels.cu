@@ -640,12 +640,13 @@ PassFn lookup_pass(int V, int NW, int S, int ops, int kind) {
 
 bool pass_supported(const PassGeom &g, int ops) { return lookup_pass(g.V, g.NW, g.S, ops, g.kind) != nullptr; }
 
-PassGeom choose_geom(int64_t n_out, int T, int num_sms) {
-    // Default (profiles/r01_sweep_kx.jsonl): CTA tiles of 4 compute
-    // warps x V=49 cells/lane trading 16-deep ghosts every 16 steps (kind 4),
-    // plus a TMA producer warp, 2 stages (~101 KB), 2 CTAs per SM.  Rings too
-    // small to give every CTA a tile use 4-warp V=17 tiles exchanging every 8 steps.
-    PassGeom g{49, 4, 2, 2, 4};
+PassGeom choose_geom(int64_t n_out, int T, int num_sms, int ops) {
+    // Default (profiles/r01_sweep_kx.jsonl): CTA tiles of 4 compute warps
+    // trading 16-deep ghosts every 16 steps (kind 4) plus a TMA producer warp, 2 stages,
+    // 2 CTAs per SM; V = 49 cells per lane for the 1- and 3-op forms, V = 53 for the 2- and
+    // 4-op forms (+2.4 % / +1.2 %; V = 53 loses 10-25 % on the other two).  Rings too small
+    // to give every CTA a tile use 4-warp V=17 tiles exchanging every 8 steps.
+    PassGeom g = (ops == 2 || ops == 4) ? PassGeom{53, 4, 2, 2, 4} : PassGeom{49, 4, 2, 2, 4};
     if (n_out < (int64_t)num_sms * g.ctas_per_sm * g.tile_out(T)) g = PassGeom{17, 4, 3, 4, 3};
     return g;
 }

@@ -49,7 +49,7 @@ struct PassGeom {
 bool pass_supported(const PassGeom &g, int ops);
 
 // Pick the pass-kernel configuration for (n, T).
-PassGeom choose_geom(int64_t n_out, int T, int num_sms);
+PassGeom choose_geom(int64_t n_out, int T, int num_sms, int ops);
 
 // K2: T fused Jacobi steps over outputs [out_lo, out_hi) of a slab.
 // A, B point at cell 0 of padded slab buffers (ghost cells at negative

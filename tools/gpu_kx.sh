@@ -1,6 +1,4 @@
-mkdir -p gpurun_out/kx13
-HEAT1D_GEOM=49,4,2,2,6 timeout 600 python -m pytest tests -m gpu -q -x -k "c1_bitwise or cross_T or ragged_multi" > gpurun_out/kx13/pytest.log 2>&1; echo pytest=$?
-for m in fast matched; do
-timeout 900 python tools/sweep.py --N 268435456 --nt 384 --T 64 96 128 --k 0.5 0.4 --mode $m --reps 3 \
-  --geoms 49,4,2,2,4 49,4,2,2,6 >> gpurun_out/kx13/sweep.jsonl 2>> gpurun_out/kx13/sweep.err; echo sweep_$m=$?
-done
+mkdir -p gpurun_out/kx14
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/kx14/smoke.log 2>&1; echo smoke=$?
+timeout 900 python -m pytest tests -m gpu -q -x -k "c3_ or c4_first or geometries or interwarp or random" > gpurun_out/kx14/pytest.log 2>&1; echo pytest=$?
+for c in C3 C4; do timeout 600 python bench.py --config $c --no-cpu-baseline --no-e2e | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', round(d['value']), d['roofline']['kernel'], round(d['other_mode']['value']), d['other_mode']['roofline']['kernel'])"; done
