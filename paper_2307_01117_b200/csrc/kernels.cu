@@ -589,7 +589,7 @@ PassFn pass_fn(int kind) {
 }
 
 // kinds 3 and 4 (inter-warp ghost exchange) for all four arithmetic variants
-#define HEAT1D_GEOMS_X(X) X(17, 4, 3) X(17, 8, 3) X(25, 4, 3) X(25, 8, 2) X(33, 6, 2) X(33, 4, 2) X(33, 4, 3) X(33, 8, 2) X(33, 8, 3) X(41, 4, 2) X(49, 4, 2) X(49, 8, 2) X(53, 4, 2) X(65, 4, 2)
+#define HEAT1D_GEOMS_X(X) X(17, 4, 3) X(17, 8, 3) X(25, 4, 3) X(25, 8, 2) X(33, 6, 2) X(33, 4, 2) X(33, 4, 3) X(33, 8, 2) X(33, 8, 3) X(41, 4, 2) X(45, 4, 2) X(47, 4, 2) X(49, 4, 2) X(49, 8, 2) X(51, 4, 2) X(53, 4, 2) X(55, 4, 2) X(65, 4, 2)
 
 template <int V, int NW, int S, int KX>
 PassFn pass_fn_x(int ops) {
@@ -641,12 +641,14 @@ PassFn lookup_pass(int V, int NW, int S, int ops, int kind) {
 bool pass_supported(const PassGeom &g, int ops) { return lookup_pass(g.V, g.NW, g.S, ops, g.kind) != nullptr; }
 
 PassGeom choose_geom(int64_t n_out, int T, int num_sms, int ops) {
-    // Default (profiles/r01_sweep_kx.jsonl): CTA tiles of 4 compute warps
-    // trading 16-deep ghosts every 16 steps (kind 4) plus a TMA producer warp, 2 stages,
-    // 2 CTAs per SM; V = 49 cells per lane for the 1- and 3-op forms, V = 53 for the 2- and
-    // 4-op forms (+2.4 % / +1.2 %; V = 53 loses 10-25 % on the other two).  Rings too small
-    // to give every CTA a tile use 4-warp V=17 tiles exchanging every 8 steps.
-    PassGeom g = (ops == 2 || ops == 4) ? PassGeom{53, 4, 2, 2, 4} : PassGeom{49, 4, 2, 2, 4};
+    // Default (profiles/r01_sweep_kx.jsonl): CTA tiles of 4 compute warps x
+    // V = 51 cells per lane trading 16-deep ghosts every 16 steps (kind 4), plus a TMA
+    // producer warp, 2 stages, 2 CTAs per SM.  V = 45..55 swept for all four arithmetic
+    // forms: 51 is best or within 0.3 % of best for each (V >= 53 spills the 1-/3-op forms
+    // to one CTA per SM).  Rings too small to give every CTA a tile use 4-warp V=17 tiles
+    // exchanging every 8 steps.
+    (void)ops;
+    PassGeom g{51, 4, 2, 2, 4};
     if (n_out < (int64_t)num_sms * g.ctas_per_sm * g.tile_out(T)) g = PassGeom{17, 4, 3, 4, 3};
     return g;
 }
