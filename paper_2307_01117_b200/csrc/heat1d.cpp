@@ -518,6 +518,8 @@ int setup_multi_resident(heat1d_t h, bool local_fits) {
         cudaGetLastError();
         return set_error(h, HEAT1D_ENOMEM, "resident scratch");
     }
+    CK(heat1d::resident_scratch_init(h->res_scratch, h->T, h->num_sms, h->comm));
+    CK(cudaStreamSynchronize(h->comm));
     return HEAT1D_OK;
 }
 
@@ -1009,6 +1011,12 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
             cudaGetLastError();
             set_error(nullptr, HEAT1D_ENOMEM, "resident scratch");
             return bail(HEAT1D_ENOMEM);
+        }
+        if (heat1d::resident_scratch_init(h->res_scratch, h->T, h->num_sms, h->stream) != cudaSuccess ||
+            cudaStreamSynchronize(h->stream) != cudaSuccess) {
+            cudaGetLastError();
+            set_error(nullptr, HEAT1D_ECUDA, "resident scratch init");
+            return bail(HEAT1D_ECUDA);
         }
     }
     *out = h;

@@ -112,6 +112,7 @@ cudaError_t launch_mbox_init(double *mbox, cudaStream_t st);
 int64_t resident_capacity(int T, int num_sms);
 bool resident_fits(int ops, int64_t n, int T, int num_sms, bool mbox = false);  // plan + co-residency
 size_t resident_scratch_bytes(int T, int num_sms);
+cudaError_t resident_scratch_init(void *scratch, int T, int num_sms, cudaStream_t st);
 cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
                             double r, void *scratch, int num_sms, cudaStream_t st, int *warps_out,
                             const MboxArgs &mb = MboxArgs{});
