@@ -6,22 +6,28 @@
         --master-port P bench.py --gpus N ...
     python bench.py --impl reference ...      # the CPU oracle on a bounded sample
 
+`--gpus N` outside torchrun re-launches itself under torch.distributed.run with N
+ranks (one per GPU, NCCL_DEBUG=INFO so the communicator's rank count is logged);
+it exits non-zero if fewer than N GPUs are visible.
+
 A step is one full solve of the workload through the C ABI: load u0 (device
 resident copy -> state) and advance nt steps (BASELINE.json configs[3] = C4 by
 default: 2^31 cells, nt = 10,000, the ring the metric's 1/2/4/8-GPU scaling
 is quoted on).  value = N*nt*K / (max over ranks of the CUDA-event time of
-the K timed steps).  Prints ONE JSON line on rank 0.
+the K timed steps).  The headline arithmetic is matched mode (Eq. 2's own
+rounding sequence, bitwise = the oracle); fast mode is timed beside it under
+`other_mode`.  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -30,25 +36,55 @@ sys.path.insert(0, ROOT)
 METRIC = "fp64 cell-updates/sec (GLUPS) at 1/2/4/8 B200 and % of HBM/FP64 roofline"
 FALLBACK_HBM_GBS = 6650.0
 SMS, FP64_LANES, SM_MHZ_MAX = 148, 64, 1965.0             # B200: fp64 lanes per SM, max SM clock
-FP64_TFLOPS = SMS * FP64_LANES * 2 * SM_MHZ_MAX * 1e6 / 1e12  # 37.2 TFLOP/s (FMA = 2 flop)
+BJ_FLOP_PER_UPDATE = 4.0                                  # BASELINE.json north_star: "4 flops per update"
+PARITY_STEPS = 100                                        # BASELINE.json configs[3]: "oracle checked on the first 100 steps"
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--steps", type=int, default=5, help="timed solves (SURVEY §8(d): 5 repetitions)")
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     p.add_argument("--T", type=int, default=0)
-    p.add_argument("--mode", default="fast", choices=["matched", "fast"],
-                   help="headline arithmetic: fast (north_star bound) or matched (bitwise = oracle)")
+    p.add_argument("--mode", default="matched", choices=["matched", "fast"],
+                   help="headline arithmetic: matched (bitwise = oracle) or fast (north_star bound)")
+    p.add_argument("--virtual-slabs", type=int, default=1,
+                   help="split each rank's ring into this many slabs on its GPU (multi-slab schedule on 1 GPU)")
+    p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"])
     p.add_argument("--no-other-mode", action="store_true", help="skip timing the other mode")
     p.add_argument("--nt", type=int, default=0, help="override the config's nt (testing only)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-parity", action="store_true", help="skip the post-run check against the oracle")
     p.add_argument("--out", default="", help="also append the JSON line to this file")
     return p.parse_args()
+
+
+# ------------------------------------------------------------------ launch
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_under_torchrun(args):
+    """--gpus N > 1 without a torchrun environment: become N ranks (one per GPU)."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.stderr.write("bench.py: --gpus %d but only %d CUDA device(s) visible\n" % (args.gpus, have))
+        sys.exit(3)
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd, env=env))
 
 
 def fp64_peak():
@@ -64,13 +100,13 @@ def fp64_peak():
         return derived, "derived: 148 SM x 64 fp64 lanes x 1.965 GHz"
 
 
-def peaks():
+def hbm_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             mp = json.load(f)
-        return float(mp["hbm_gbs"]), "measured"
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return FALLBACK_HBM_GBS, "fallback"
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
 # ------------------------------------------------------------------ clocks
@@ -128,52 +164,91 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ oracle baseline (CPU)
+def host_identity():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    try:
+        avail = len(os.sched_getaffinity(0))
+    except Exception:
+        avail = None
+    return {"cpu_model": model, "nproc": os.cpu_count(), "cores_available": avail}
+
+
+class PinOneCore:
+    """Pin the calling process to one core for the single-threaded oracle."""
+
+    def __enter__(self):
+        self.prev = None
+        self.core = None
+        try:
+            self.prev = os.sched_getaffinity(0)
+            self.core = max(self.prev)
+            os.sched_setaffinity(0, {self.core})
+        except Exception:
+            pass
+        return self
+
+    def __exit__(self, *exc):
+        if self.prev is not None:
+            try:
+                os.sched_setaffinity(0, self.prev)
+            except Exception:
+                pass
+
+
 def cpu_oracle_sample(cfg, target_s=12.0):
     """Time the oracle (O3 light-cone window == O1 on the window) on a contiguous
-    window of the workload's ring for its first steps, single-threaded."""
-    import numpy as np
+    window of the workload's ring for its first steps, single-threaded, pinned."""
     import oracle
     r = oracle.r_of(cfg.k, cfg.dt, cfg.dx)
     t = min(cfg.nt, 100)
     m = min(cfg.N, 1 << 20)
-    w0 = cfg.u0(0 - t, m + 2 * t) if cfg.N >= m + 2 * t else None
-    if w0 is None:  # tiny ring: whole-ring O1
-        u0 = cfg.u0()
+    with PinOneCore() as pin:
+        if cfg.N < m + 2 * t:  # tiny ring: whole-ring O1
+            u0 = cfg.u0()
+            t0 = time.perf_counter()
+            oracle.run(u0, r, cfg.nt)
+            dt = time.perf_counter() - t0
+            return cfg.N * cfg.nt / dt / 1e9, "whole ring N=%d x %d steps (O1)" % (cfg.N, cfg.nt), pin.core
+        w0 = cfg.u0(0 - t, m + 2 * t)
         t0 = time.perf_counter()
-        oracle.run(u0, r, cfg.nt)
+        oracle.window(w0, t, r)
         dt = time.perf_counter() - t0
-        return cfg.N * cfg.nt / dt / 1e9, "whole ring N=%d x %d steps (O1)" % (cfg.N, cfg.nt)
-    # calibrate, then scale the window to ~target_s
-    t0 = time.perf_counter()
-    oracle.window(w0, t, r)
-    dt = time.perf_counter() - t0
-    upd = (m + t) * t
-    rate = upd / dt
-    m2 = int(min(cfg.N - 2 * t, max(m, rate * target_s / t - t)))
-    m2 = max(1024, m2)
-    w0 = cfg.u0(0 - t, m2 + 2 * t)
-    t0 = time.perf_counter()
-    oracle.window(w0, t, r)
-    dt = time.perf_counter() - t0
+        rate = (m + t) * t / dt
+        m2 = int(min(cfg.N - 2 * t, max(m, rate * target_s / t - t)))
+        m2 = max(1024, m2)
+        w0 = cfg.u0(0 - t, m2 + 2 * t)
+        t0 = time.perf_counter()
+        oracle.window(w0, t, r)
+        dt = time.perf_counter() - t0
     upd = sum(m2 + 2 * (t - s) - 2 for s in range(t))  # cells updated per shrinking step
     return upd / dt / 1e9, "O3 window of %d cells x first %d steps of %s (%.3g updates, %.1f s)" % (
-        m2, t, cfg.name, upd, dt)
+        m2, t, cfg.name, upd, dt), pin.core
 
 
-def host_cores_used():
-    return 1  # the oracle is a plain single-threaded C loop
+def cpu_baseline_obj(value, sample, core):
+    d = {"value": value, "unit": "GLUPS", "cores": 1, "kind": "oracle", "sample": sample,
+         "threads": 1, "pinned_core": core}
+    d.update(host_identity())
+    return d
 
 
 def reference_arm(args, cfg, rank):
-    """--impl reference: the oracle as it stands, on rank 0's host cores."""
+    """--impl reference: the oracle as it stands, on rank 0's host cores (one pinned core)."""
     if rank != 0:
         return
     import oracle
     oracle.build()
     vals = []
-    sample = ""
+    sample, core = "", None
     for i in range(args.warmup + args.steps):
-        v, sample = cpu_oracle_sample(cfg, target_s=4.0)
+        v, sample, core = cpu_oracle_sample(cfg, target_s=4.0)
         if i >= args.warmup:
             vals.append(v)
     value = statistics.median(vals)
@@ -184,8 +259,7 @@ def reference_arm(args, cfg, rank):
         "config": {"workload": cfg.name, "N": cfg.N, "nx": cfg.nx, "np": cfg.np, "nt": cfg.nt, "k": cfg.k,
                    "dt": cfg.dt, "dx": cfg.dx, "mode": "oracle (canonical order, bitwise = matched mode)",
                    "parallelism": "cpu, 1 core"},
-        "cpu_baseline": {"value": value, "unit": "GLUPS", "cores": host_cores_used(), "kind": "oracle",
-                         "sample": sample},
+        "cpu_baseline": cpu_baseline_obj(value, sample, core),
         "e2e": {"value": value, "unit": "GLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -200,40 +274,49 @@ def emit(line, args):
             f.write(s + "\n")
 
 
-# ------------------------------------------------------------------ GPU arm
-def kernel_roofline(info, cfg, count, world, steps, k2_launches, k2_ms, ms, value, mode):
-    """Roofline of the dominant kernel (K2 pass or K6 whole solve), this rank."""
-    if not k2_launches:
+# ------------------------------------------------------------------ roofline
+def flops_executed(dp_ops, steps_per_pass):
+    """fp64 flops the kernel's arithmetic executes per update (FMA = 2): the 4-op and 3-op
+    matched forms and the literal form compute Eq. 2's 5 flops; the scaled fast forms 1 (r=1/2)
+    or 3 (+ one rescale DMUL per cell per pass)."""
+    return {1: 1.0, 2: 3.0}.get(dp_ops, 5.0) + (1.0 / steps_per_pass if dp_ops <= 2 else 0.0)
+
+
+def kernel_roofline(info, cfg, count, world, steps, k_launches, k_ms, ms, value, mode):
+    """Roofline of the dominant kernel (K2 pass or K6 whole solve), as SURVEY §8(d) /
+    BASELINE.json north_star define it: min(HBM / (16/T B), FP64 peak / 4 flop) per update."""
+    if not k_launches:
         return None
-    hbm, peak_kind = peaks()
-    T = info["T"]
-    avg_ms = k2_ms / k2_launches
-    upd_launch = count * cfg.nt * steps / k2_launches       # cell updates per launch, this rank
-    steps_per_pass = cfg.nt if info["resident"] else T       # steps per HBM round trip of the state
-    alg_bytes = 16.0 * count * (upd_launch / count) / steps_per_pass  # 8 B read + 8 B written per cell per pass
-    hbm_term = hbm / (16.0 / steps_per_pass)                 # GLUPS bound by HBM (BASELINE.json)
-    fp64_term = FP64_TFLOPS * 1e3 / 4.0                      # GLUPS bound by FP64 peak / 4 flop
-    bj_roof = min(hbm_term, fp64_term) * world
-    kind = info["pass_kind"]
-    k6v = 17 if T <= 32 else 33 if T <= 64 else 49          # resident.cu rv_of(T)
-    kernel = ("k6_resident<V=%d>" % k6v if info["resident"] else
-              ["k2_pass", "k2w_pass", "k2p_pass", "k2p_pass", "k2p_pass"][kind] + "<V=%d,NW=%d,S=%d%s>" % (
-                  info["pass_V"], info["pass_NW"], info["pass_S"],
-                  {3: ",KX=8", 4: ",KX=16"}.get(kind, ""))) + "<OPS=%d>" % info["dp_ops"]
-    # the kernel's own bounds: HBM (16 B per cell per pass) and the fp64 pipe's issue rate
-    # 148 SM x 64 lanes x 1.965 GHz against its algorithmic fp64 instructions per update
-    # (dp_ops; the scaled fast variants add one rescale DMUL per cell per pass, DESIGN.md §6)
-    inst_per_upd = info["dp_ops"] + (1.0 / steps_per_pass if info["dp_ops"] <= 2 else 0.0)
+    hbm, hbm_kind = hbm_peak()
     pipe, pipe_kind = fp64_peak()                            # T fp64 lane-instructions / s
-    alu_term = pipe * 1e3 / inst_per_upd                     # GLUPS
-    achieved_gbs = alg_bytes / (avg_ms / 1e3) / 1e9
-    dpi = inst_per_upd * upd_launch / (avg_ms / 1e3) / 1e12
-    if hbm_term <= alu_term:
+    fp64_tflops = 2.0 * pipe                                 # FMA = 2 flop
+    T = info["T"]
+    avg_ms = k_ms / k_launches
+    upd_launch = count * cfg.nt * steps / k_launches         # cell updates per launch, this rank
+    steps_per_pass = cfg.nt if info["resident"] else T       # steps per HBM round trip of the state
+    alg_bytes = 16.0 * upd_launch / steps_per_pass           # 8 B read + 8 B written per cell per pass
+    hbm_glups = hbm / (16.0 / steps_per_pass)                # GLUPS bound by HBM
+    fp64_glups = fp64_tflops * 1e3 / BJ_FLOP_PER_UPDATE      # GLUPS bound by FP64 peak / 4 flop
+    secs = avg_ms / 1e3
+    achieved_gbs = alg_bytes / secs / 1e9
+    achieved_tflops = BJ_FLOP_PER_UPDATE * upd_launch / secs / 1e12
+    if hbm_glups <= fp64_glups:
         roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
-                "frac": achieved_gbs / hbm, "peak_kind": peak_kind}
+                "frac": achieved_gbs / hbm, "peak_kind": hbm_kind}
     else:
-        roof = {"bound": "alu", "achieved": dpi, "peak": pipe, "unit": "Tinst/s (fp64 DFMA/DADD/DMUL)",
-                "frac": dpi / pipe, "peak_kind": pipe_kind}
+        roof = {"bound": "alu", "achieved": achieved_tflops, "peak": fp64_tflops,
+                "unit": "TFLOP/s (4 flop/update, SURVEY §8(d))", "frac": achieved_tflops / fp64_tflops,
+                "peak_kind": pipe_kind + " x 2 flop/FMA"}
+    kind = info["pass_kind"]
+    k6v = 17 if T <= 32 else 33 if T <= 64 else 49            # resident.cu rv_of(T)
+    kernel = ("k6_resident<V=%d>" % k6v if info["resident"] else
+              "k2p_pass<V=%d,NW=%d,S=%d,KX=%d>" % (info["pass_V"], info["pass_NW"], info["pass_S"],
+                                                   8 if kind == 3 else 16)) + "<OPS=%d>" % info["dp_ops"]
+    # the kernel's own bound: fp64 instructions it must issue per update (dp_ops; the scaled
+    # fast variants add one rescale DMUL per cell per pass) against the fp64 pipe's issue rate
+    inst_per_upd = info["dp_ops"] + (1.0 / steps_per_pass if info["dp_ops"] <= 2 else 0.0)
+    dpi = inst_per_upd * upd_launch / secs / 1e12
+    flops_x = flops_executed(info["dp_ops"], steps_per_pass)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -241,19 +324,21 @@ def kernel_roofline(info, cfg, count, world, steps, k2_launches, k2_ms, ms, valu
     except Exception:
         pass
     roof.update({
-        "traffic": traffic, "kernel": kernel, "launches": k2_launches, "avg_launch_ms": avg_ms,
-        "steps_per_launch": upd_launch / count,
-        "alg_bytes_per_launch": alg_bytes, "alg_fp64_inst_per_launch": inst_per_upd * upd_launch,
-        "fp64_inst_per_update": inst_per_upd, "hbm_gbs_achieved": achieved_gbs,
-        "hbm_frac": achieved_gbs / hbm, "fp64_pipe_frac": dpi / pipe,
-        "kernel_roofline_glups": min(hbm_term, alu_term) * world,
-        "baseline_json_roofline_glups": bj_roof,
-        "baseline_json_frac": value / bj_roof,
-        "baseline_json_bound": "hbm" if hbm_term < fp64_term else "fp64 (37.2 TFLOP/s / 4 flop)",
-        "kernel_share_of_step": k2_ms / ms if world == 1 else None})
+        "traffic": traffic, "kernel": kernel, "launches": k_launches, "avg_launch_ms": avg_ms,
+        "steps_per_launch": upd_launch / count, "updates_per_launch": upd_launch,
+        "alg_bytes_per_launch": alg_bytes, "alg_flop_per_launch": BJ_FLOP_PER_UPDATE * upd_launch,
+        "roofline_glups": min(hbm_glups, fp64_glups) * world,
+        "hbm_gbs_achieved": achieved_gbs, "hbm_frac": achieved_gbs / hbm,
+        # what the kernel itself executes (not §8(d)'s algorithmic count)
+        "fp64_inst_per_update": inst_per_upd, "fp64_flop_per_update_executed": flops_x,
+        "reduced_op_form": flops_x < BJ_FLOP_PER_UPDATE,
+        "fp64_pipe_frac": dpi / pipe,
+        "kernel_issue_bound_glups": min(hbm_glups, pipe * 1e3 / inst_per_upd) * world,
+        "kernel_share_of_step": k_ms / ms if world == 1 else None})
     return roof
 
 
+# ------------------------------------------------------------------ GPU arm
 def fresh_nccl_id(h1, world, rank):
     """One ncclUniqueId per communicator (each handle owns one), broadcast from rank 0."""
     if world == 1:
@@ -264,86 +349,148 @@ def fresh_nccl_id(h1, world, rank):
     return obj[0]
 
 
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(x if isinstance(x, list) else [x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    v = t.tolist()
+    return v if isinstance(x, list) else v[0]
+
+
+def timed_steps(fn, steps, stream, world):
+    """K back-to-back calls bracketed by barrier + synchronize, CUDA events on `stream` around
+    each; returns (total ms, per-step ms), both max over ranks."""
+    import torch
+    import torch.distributed as dist
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs[0].record(stream)
+    for i in range(steps):
+        fn()
+        evs[i + 1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    per = [evs[i].elapsed_time(evs[i + 1]) for i in range(steps)]
+    total = evs[0].elapsed_time(evs[steps])
+    both = max_over_ranks([total] + per, world)
+    return both[0], both[1:]
+
+
+def step_stats(per, updates_per_step):
+    return {"ms_median": statistics.median(per), "ms_min": min(per), "ms_max": max(per),
+            "glups_median": updates_per_step / (statistics.median(per) / 1e3) / 1e9,
+            "glups_best": updates_per_step / (min(per) / 1e3) / 1e9, "ms_all": per}
+
+
 def measure(h1, cfg, mode, args, world, rank, local_rank, stream, u0_dev, with_e2e, sampler_on):
     """Time K steps (after W warm-ups) of one full solve in `mode`; max over ranks."""
     import torch
-    import torch.distributed as dist
     h = h1.Heat1D(cfg.nx, cfg.np, cfg.nt, cfg.k, cfg.dt, cfg.dx, T=args.T, mode=mode, rank=rank,
-                  nranks=world, nccl_id=fresh_nccl_id(h1, world, rank), device=local_rank, stream=stream)
+                  nranks=world, nccl_id=fresh_nccl_id(h1, world, rank), device=local_rank, stream=stream,
+                  virtual_slabs=args.virtual_slabs, transport=args.transport)
     first, count = h.local_range
 
     def step():
         h.set_initial(u0_dev)
         h.run(cfg.nt)
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
 
-    sampler = ClockSampler(range(world)) if (rank == 0 and sampler_on) else None
+    sampler = ClockSampler(range(torch.cuda.device_count())) if (rank == 0 and sampler_on) else None
     launches0 = h.info()["launches"]
     h.set_profiling(True)
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    barrier()
-    torch.cuda.synchronize()
     if sampler:
         sampler.start()
         time.sleep(0.3)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
+    ms, per = timed_steps(step, args.steps, stream, world)
     clocks = sampler.stop() if sampler else None
-    ms = ev0.elapsed_time(ev1)
-    k2_launches, k2_ms = h.profile()
+    k_launches, k_ms = h.profile()
     h.set_profiling(False)
     launches = h.info()["launches"] - launches0
     info = h.info()
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    updates = cfg.N * cfg.nt * args.steps
-    value = updates / (ms / 1e3) / 1e9
+    updates = cfg.N * cfg.nt
+    value = updates * args.steps / (ms / 1e3) / 1e9
 
-    # ---- end to end: pinned host u0 -> set_initial -> run -> get -> pinned host
+    # ---- end to end through the C ABI from/to pinned HOST memory (copies inside the timed region)
     e2e = None
     if with_e2e:
         host_in = torch.empty(count, dtype=torch.float64, pin_memory=True)
         host_out = torch.empty(count, dtype=torch.float64, pin_memory=True)
         host_in.copy_(u0_dev)
         torch.cuda.synchronize()
-        barrier()
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
+
+        def plain():
+            h.set_initial(host_in)
+            h.run(cfg.nt)
+            h.get(host_out)
+
+        def windows():
             h.solve_host(host_in, cfg.nt, host_out)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        ems = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
-        e2e = {"value": updates / (ems / 1e3) / 1e9, "unit": "GLUPS", "h2d_bytes_per_step": 8 * count,
-               "d2h_bytes_per_step": 8 * count, "ms_per_step": ems / args.steps,
-               "path": "heat1d_solve_host(pinned host u0 -> nt steps -> pinned host out)",
-               "windows": h.info()["stream_windows"]}
+
+        res = {}
+        for name, fn in (("set_initial+run+get", plain), ("solve_host", windows)):
+            ems, eper = timed_steps(fn, args.steps, stream, world)
+            res[name] = {"value": updates * args.steps / (ems / 1e3) / 1e9, "ms_per_step": ems / args.steps,
+                         "windows": h.info()["stream_windows"] if name == "solve_host" else 0}
+        # the headline e2e: at one rank the light-cone-window solve (transfers hidden behind the
+        # compute); across ranks the plain sequence, whose run() exchanges depth-T halos every T
+        # steps (the multi-rank solve_host trades nt-deep halos once instead)
+        head = "solve_host" if world == 1 else "set_initial+run+get"
+        e2e = {"value": res[head]["value"], "unit": "GLUPS", "h2d_bytes_per_step": 8 * count,
+               "d2h_bytes_per_step": 8 * count, "ms_per_step": res[head]["ms_per_step"],
+               "path": {"solve_host": "heat1d_solve_host(pinned host u0 -> nt steps -> pinned host out): "
+                                      "light-cone windows, H2D/D2H overlapped with compute",
+                        "set_initial+run+get": "heat1d_set_initial(pinned host) + heat1d_run(nt) + "
+                                               "heat1d_get(pinned host)"}[head],
+               "variants": res}
         del host_in, host_out
-    roof = kernel_roofline(info, cfg, count, world, args.steps, k2_launches, k2_ms, ms, value, mode)
-    h.close()
-    return {"value": value, "ms": ms, "info": info, "roof": roof, "e2e": e2e, "clocks": clocks,
-            "launches": launches}
+    roof = kernel_roofline(info, cfg, count, world, args.steps, k_launches, k_ms, ms, value, mode)
+    return {"value": value, "ms": ms, "per": per, "info": info, "roof": roof, "e2e": e2e, "clocks": clocks,
+            "launches": launches, "handle": h, "first": first, "count": count}
+
+
+def parity_check(h1, h, cfg, u0_dev, first, count, world, mode):
+    """After the timed region: the first min(nt, 100) steps of the same handle vs the oracle's
+    light-cone windows (O3) at both ends of this rank's slab (the slab boundaries, where the
+    halo exchange acts) and in its middle.  Matched: bitwise; fast: north_star's bound."""
+    import numpy as np
+    import oracle
+    t = min(cfg.nt, PARITY_STEPS)
+    r = oracle.r_of(cfg.k, cfg.dt, cfg.dx)
+    import torch
+    h.set_initial(u0_dev)
+    h.run(t)
+    got_dev = torch.empty(count, dtype=torch.float64, device="cuda")
+    h.get(got_dev)
+    w = min(count, 4096)
+    bad = 0
+    checked = 0
+    worst = 0.0
+    bound = 0.0
+    for a in sorted({0, max(0, count // 2 - w // 2), count - w}):
+        w0 = cfg.u0(first + a - t, w + 2 * t)
+        want = oracle.window(w0, t, r)
+        g = got_dev[a:a + w].cpu().numpy()
+        checked += w
+        if mode == "matched":
+            bad += int(np.count_nonzero(g.view(np.uint64) != want.view(np.uint64)))
+        else:
+            worst = max(worst, float(np.max(np.abs(g - want))))
+            bound = max(bound, 1e-12 * float(np.max(np.abs(w0))) * t)
+    del got_dev
+    ok = bad == 0 if mode == "matched" else worst <= bound
+    ok_all = max_over_ranks(0.0 if ok else 1.0, world) == 0.0
+    return {"steps": t, "cells_checked_per_rank": checked, "windows": "O3 at slab start, middle, end (every rank)",
+            "criterion": "bitwise" if mode == "matched" else "<= 1e-12*max|u0|*t", "ok": bool(ok_all),
+            "mismatches_rank0": bad, "max_abs_err_rank0": worst}
 
 
 def main():
@@ -353,6 +500,7 @@ def main():
     if args.nt:
         from dataclasses import replace
         cfg = replace(cfg, nt=args.nt)
+    in_torchrun = "WORLD_SIZE" in os.environ
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -360,6 +508,11 @@ def main():
     if args.impl == "reference":
         reference_arm(args, cfg, rank)
         return
+    if args.gpus > 1 and not in_torchrun:
+        relaunch_under_torchrun(args)
+    if in_torchrun and world != args.gpus:
+        sys.stderr.write("bench.py: WORLD_SIZE=%d but --gpus %d\n" % (world, args.gpus))
+        sys.exit(3)
 
     import torch
     import torch.distributed as dist
@@ -367,6 +520,9 @@ def main():
     _build.build()
     import paper_2307_01117_b200 as h1
 
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
@@ -384,13 +540,18 @@ def main():
         u0_dev.copy_(torch.from_numpy(cfg.u0(first, count)))
     torch.cuda.synchronize()
 
-    main_m = measure(h1, cfg, args.mode, args, world, rank, local_rank, stream, u0_dev,
-                     not args.no_e2e, True)
+    main_m = measure(h1, cfg, args.mode, args, world, rank, local_rank, stream, u0_dev, not args.no_e2e, True)
+    parity = None
+    if not args.no_parity:
+        parity = parity_check(h1, main_m["handle"], cfg, u0_dev, first, count, world, args.mode)
+    main_m["handle"].close()
     other = None
     if not args.no_other_mode:
         om = "matched" if args.mode == "fast" else "fast"
         o = measure(h1, cfg, om, args, world, rank, local_rank, stream, u0_dev, False, False)
+        o["handle"].close()
         other = {"mode": om, "value": o["value"], "ms_per_step": o["ms"] / args.steps,
+                 "step_stats": step_stats(o["per"], cfg.N * cfg.nt),
                  "dp_ops": o["info"]["dp_ops"], "T": o["info"]["T"], "gpu_launches": o["launches"],
                  "roofline": o["roof"],
                  "parity": "bitwise = oracle" if om == "matched" else "<= 1e-12*max|u0|*nt vs oracle"}
@@ -399,13 +560,14 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            v, sample = cpu_oracle_sample(cfg)
-            cpu = {"value": v, "unit": "GLUPS", "cores": host_cores_used(), "kind": "oracle", "sample": sample}
+            v, sample, core = cpu_oracle_sample(cfg)
+            cpu = cpu_baseline_obj(v, sample, core)
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "GLUPS", "cores": 1, "kind": "oracle", "sample": "failed: %s" % e}
 
     if rank == 0:
         ms = main_m["ms"]
+        nslab = world * args.virtual_slabs
         line = {
             "metric": METRIC, "value": main_m["value"], "unit": "GLUPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -413,17 +575,20 @@ def main():
             "data": "synthetic (BASELINE.json %s recipe, seeded)" % cfg.name,
             "config": {"workload": cfg.name, "N": cfg.N, "nx": cfg.nx, "np": cfg.np, "nt": cfg.nt, "k": cfg.k,
                        "dt": cfg.dt, "dx": cfg.dx, "r": info["r"], "T": info["T"], "mode": args.mode,
-                       "parity": ("bitwise = oracle" if args.mode == "matched"
+                       "parity": ("bitwise = oracle (Eq. 2's rounding sequence)" if args.mode == "matched"
                                   else "<= 1e-12*max|u0|*nt vs oracle (north_star fast-mode bound)"),
-                       "dp_ops": info["dp_ops"], "parallelism": "slabs%d" % world,
-                       "halo_transport": ("none (one slab)" if world == 1 else
+                       "dp_ops": info["dp_ops"], "parallelism": "slabs%d" % nslab,
+                       "ranks": world, "virtual_slabs_per_rank": args.virtual_slabs,
+                       "halo_transport": ("none (one slab)" if nslab == 1 else
                                           "k6 mailbox (NVLink peer memory)" if info["resident"] else
-                                          ["nccl send/recv", "p2p puts from K3 (NVLink peer memory)"][info["transport"]]),
+                                          ["nccl send/recv" if world > 1 else "device copies + K3",
+                                           "p2p puts from K3 (peer memory)"][info["transport"]]),
                        "l2": "inputs larger than L2" if 16 * cfg.N // world > 126 * 2 ** 20
                        else "L2-resident ring (no flush; each step re-reads u0 from HBM copy)",
                        "tile_cells": info["tile_cells"], "grid": info["grid"]},
-            "roofline": main_m["roof"], "other_mode": other, "cpu_baseline": cpu, "e2e": main_m["e2e"],
-            "clocks": main_m["clocks"], "gpu_launches": main_m["launches"],
+            "step_stats": step_stats(main_m["per"], cfg.N * cfg.nt),
+            "roofline": main_m["roof"], "other_mode": other, "parity_check": parity, "cpu_baseline": cpu,
+            "e2e": main_m["e2e"], "clocks": main_m["clocks"], "gpu_launches": main_m["launches"],
         }
         emit(line, args)
     if world > 1:

@@ -48,18 +48,21 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = "", defines=()) -> str:
+    """Compile libheat1d.so (or, for measurement builds, `out` with extra -D`defines`)."""
+    target = out or LIB
+    if not out and not force and up_to_date():
         return LIB
     inc, lib = nccl_dirs()
     nvcc = os.environ.get("NVCC", "nvcc")
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     common = [nvcc, "-std=c++17", "-O3", *ARCH, "-lineinfo", "-Xptxas", "-v",
-              "-Xcompiler", "-fPIC,-fvisibility=hidden", "-DHEAT1D_BUILD", "-I", INCLUDE, "-I", CSRC, "-I", inc]
+              "-Xcompiler", "-fPIC,-fvisibility=hidden", "-DHEAT1D_BUILD", "-I", INCLUDE, "-I", CSRC, "-I", inc,
+              *["-D" + d for d in defines]]
 
     def compile_one(src):
-        obj = os.path.join(objdir, os.path.basename(src) + ".%d.o" % os.getpid())
+        obj = os.path.join(objdir, os.path.basename(src) + ".%d.%d.o" % (os.getpid(), abs(hash(target)) % 10000))
         cmd = common + ["-c", src, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         return obj, " ".join(cmd) + "\n" + res.stdout + res.stderr, res.returncode
@@ -69,7 +72,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=len(sources())) as ex:
         results = list(ex.map(compile_one, sources()))
     log = "".join(r[1] for r in results)
-    tmp = LIB + ".tmp%d" % os.getpid()
+    tmp = target + ".tmp%d" % os.getpid()
     ok = all(r[2] == 0 for r in results)
     if ok:
         cmd = [nvcc, *ARCH, "-shared", *[r[0] for r in results], "-o", tmp,
@@ -80,15 +83,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for r in results:
         if os.path.exists(r[0]):
             os.remove(r[0])
-    with open(os.path.join(HERE, "build.log"), "w") as f:
+    os.makedirs(objdir, exist_ok=True)
+    with open(os.path.join(objdir, "build.log" if not out else os.path.basename(out) + ".log"), "w") as f:
         f.write(log)
     if not ok:
         sys.stderr.write(log)
-        raise RuntimeError("nvcc failed (see paper_2307_01117_b200/build.log)")
+        raise RuntimeError("nvcc failed (see paper_2307_01117_b200/build/build.log)")
     if verbose:
         sys.stderr.write(log)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -178,6 +178,9 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 int64_t pad_for(int T) { return round_up((int64_t)T + 2, 16); }
 
+// Exactness guard (stencil.cuh, DESIGN.md c3) of a block of Tp steps in arithmetic `ops`.
+heat1d::Guard guard_for(heat1d_t h, int ops, int Tp);
+
 // Plain partition arithmetic (also exported as heat1d_partition).
 int partition(int64_t nx, int64_t np, int32_t G, int32_t g, int64_t *first, int64_t *count) {
     if (nx < 1 || np < 1 || G < 1 || g < 0 || g >= G) return HEAT1D_EINVAL;
@@ -205,6 +208,39 @@ int64_t min_slab(int64_t nx, int64_t np, int32_t G) {
     return mn;
 }
 
+// The four halo messages of one rank (heat1d_plan_exchange): its slab of
+// `count` cells sends its last and first `depth` cells to the right and left neighbours
+// and receives their edges into its left and right ghost pads.  The single source of the
+// offsets for every exchange the library issues (exchange(), the nt-deep halos of a
+// multi-rank heat1d_solve_host).
+void make_plan(int64_t count, int64_t depth, int rank, int nranks, heat1d_exchange_plan *plan) {
+    plan->left = (rank - 1 + nranks) % nranks;
+    plan->right = (rank + 1) % nranks;
+    plan->send_right_off = count - depth;
+    plan->send_left_off = 0;
+    plan->recv_left_off = -depth;
+    plan->recv_right_off = count;
+    plan->cells = depth;
+}
+
+// Issue a plan's messages on `st` in the plan's order (matters when left == right):
+// send(right edge -> right), send(left edge -> left), recv(left pad <- left), recv(right pad
+// <- right).  `send_base` / `recv_base` hold cell 0 of the slab (they differ when the
+// caller stages the edges elsewhere, e.g. host arrays); offsets are relative to them.
+ncclResult_t issue_plan(const heat1d_exchange_plan &pl, const double *send_base, double *recv_base,
+                        ncclComm_t comm, cudaStream_t st) {
+    ncclResult_t e;
+    const size_t n = (size_t)pl.cells;
+    if ((e = ncclGroupStart()) != ncclSuccess) return e;
+    if ((e = ncclSend(send_base + pl.send_right_off, n, ncclDouble, pl.right, comm, st)) != ncclSuccess) goto end;
+    if ((e = ncclSend(send_base + pl.send_left_off, n, ncclDouble, pl.left, comm, st)) != ncclSuccess) goto end;
+    if ((e = ncclRecv(recv_base + pl.recv_left_off, n, ncclDouble, pl.left, comm, st)) != ncclSuccess) goto end;
+    e = ncclRecv(recv_base + pl.recv_right_off, n, ncclDouble, pl.right, comm, st);
+end:
+    const ncclResult_t e2 = ncclGroupEnd();
+    return e != ncclSuccess ? e : e2;
+}
+
 int auto_T(int ops) {
     // DESIGN.md §6 (T sweeps in profiles/r01_sweep_kx.jsonl, r01_c3_tsweep.md): each pass
     // moves 16/T bytes per update, so T is raised until the pass is fp64-issue bound; with
@@ -217,7 +253,7 @@ int auto_T(int ops) {
 bool parse_geom_env(PassGeom *g) {
     const char *s = getenv("HEAT1D_GEOM");  // "V,NW,S,ctas_per_sm[,kind]" (tuning knob)
     if (!s || !*s) return false;
-    int v, nw, st, c, kind = 1;
+    int v, nw, st, c, kind = 4;
     const int got = sscanf(s, "%d,%d,%d,%d,%d", &v, &nw, &st, &c, &kind);
     if (got < 4) return false;
     *g = PassGeom{v, nw, st, c, kind};
@@ -248,6 +284,10 @@ int prof_collect(heat1d_t h) {
 
 double *cell0(heat1d_t h, const Slab &s, int which) { return s.buf[which] + h->pad; }
 
+heat1d::Guard guard_for(heat1d_t h, int ops, int Tp) {
+    return heat1d::guard_of(h->mode == HEAT1D_MODE_MATCHED, ops, h->r, Tp);
+}
+
 int launch_pass_slab(heat1d_t h, const Slab &s, int Tp, int64_t lo, int64_t hi, int wrapT) {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->prof) {
@@ -258,7 +298,8 @@ int launch_pass_slab(heat1d_t h, const Slab &s, int Tp, int64_t lo, int64_t hi, 
     }
     int grid = 0;
     CK(heat1d::launch_pass(h->geom, h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp, lo, hi,
-                           wrapT, h->q, heat1d::scale_of(h->r, Tp), h->num_sms, h->stream, &grid));
+                           wrapT, h->q, heat1d::scale_of(h->r, Tp), guard_for(h, h->ops, Tp), h->num_sms,
+                           h->stream, &grid));
     if (grid > 0) h->launches++;
     h->last_grid = grid > 0 ? grid : h->last_grid;
     if (h->prof) CK(cudaEventRecord(e1, h->stream));
@@ -273,25 +314,26 @@ int exchange(heat1d_t h, int Tp) {
     if (h->nranks > 1) {
         const Slab &s = h->slabs[0];
         double *A = cell0(h, s, cur);
-        const int left = (h->rank - 1 + h->nranks) % h->nranks;
-        const int right = (h->rank + 1) % h->nranks;
-        NK(ncclGroupStart());
-        NK(ncclSend(A + s.count - Tp, (size_t)Tp, ncclDouble, right, h->nccl, h->comm));
-        NK(ncclSend(A, (size_t)Tp, ncclDouble, left, h->nccl, h->comm));
-        NK(ncclRecv(A - Tp, (size_t)Tp, ncclDouble, left, h->nccl, h->comm));
-        NK(ncclRecv(A + s.count, (size_t)Tp, ncclDouble, right, h->nccl, h->comm));
-        NK(ncclGroupEnd());
+        heat1d_exchange_plan pl;
+        make_plan(s.count, Tp, h->rank, h->nranks, &pl);
+        NK(issue_plan(pl, A, A, h->nccl, h->comm));
         return HEAT1D_OK;
     }
-    // virtual slabs on one device: the same four messages as device copies
+    // virtual slabs on one device: the same messages as device copies -- slab g's receives
+    // are its neighbours' sends of the same plan
     for (int g = 0; g < ns; ++g) {
         const Slab &s = h->slabs[g];
         const Slab &L = h->slabs[(g - 1 + ns) % ns];
         const Slab &R = h->slabs[(g + 1) % ns];
+        heat1d_exchange_plan ps, pL, pR;
+        make_plan(s.count, Tp, g, ns, &ps);
+        make_plan(L.count, Tp, (g - 1 + ns) % ns, ns, &pL);
+        make_plan(R.count, Tp, (g + 1) % ns, ns, &pR);
         double *A = cell0(h, s, cur);
-        CK(cudaMemcpyAsync(A - Tp, cell0(h, L, cur) + L.count - Tp, (size_t)Tp * 8, cudaMemcpyDeviceToDevice,
-                           h->comm));
-        CK(cudaMemcpyAsync(A + s.count, cell0(h, R, cur), (size_t)Tp * 8, cudaMemcpyDeviceToDevice, h->comm));
+        CK(cudaMemcpyAsync(A + ps.recv_left_off, cell0(h, L, cur) + pL.send_right_off, (size_t)Tp * 8,
+                           cudaMemcpyDeviceToDevice, h->comm));
+        CK(cudaMemcpyAsync(A + ps.recv_right_off, cell0(h, R, cur) + pR.send_left_off, (size_t)Tp * 8,
+                           cudaMemcpyDeviceToDevice, h->comm));
     }
     return HEAT1D_OK;
 }
@@ -318,7 +360,8 @@ int run_resident(heat1d_t h, int64_t nt) {
         h->k6_base += (unsigned)((nt + h->T - 1) / h->T) + 2u;
     }
     CK(heat1d::launch_resident(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, h->T, nt, h->q,
-                               h->r, h->res_scratch, h->num_sms, h->stream, &h->res_warps, mb));
+                               h->r, guard_for(h, h->ops, h->T), h->res_scratch, h->num_sms, h->stream,
+                               &h->res_warps, mb));
     h->launches++;
     if (h->prof) CK(cudaEventRecord(e1, h->stream));
     h->cur ^= 1;
@@ -341,8 +384,9 @@ int run_passes(heat1d_t h, int64_t nt) {
                 e1 = prof_event(h);
                 CK(cudaEventRecord(e0, h->stream));
             }
-            // one step per launch: the scaled variants degenerate to their unscaled fast form
-            CK(heat1d::launch_naive(heat1d::ops_scaled(h->ops) ? 3 : h->ops, cell0(h, s, h->cur),
+            // one step per launch: matched mode runs the oracle's literal sequence (OPS 5), fast
+            // mode the contracted 3-op form
+            CK(heat1d::launch_naive(h->mode == HEAT1D_MODE_MATCHED ? 5 : 3, cell0(h, s, h->cur),
                                     cell0(h, s, h->cur ^ 1), s.count, h->r, h->stream));
             if (h->prof) CK(cudaEventRecord(e1, h->stream));
             h->launches++;
@@ -382,7 +426,8 @@ int run_passes(heat1d_t h, int64_t nt) {
                 }
                 for (const Slab &s : h->slabs) {
                     CK(heat1d::launch_edges_put(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp,
-                                                h->q, heat1d::scale_of(h->r, Tp), s.flags, h->xg,
+                                                h->q, heat1d::scale_of(h->r, Tp), guard_for(h, h->ops, Tp),
+                                                s.flags, h->xg,
                                                 s.put_left[h->cur ^ 1], s.put_right[h->cur ^ 1], s.nflag_left,
                                                 s.nflag_right, h->comm));
                     h->launches++;
@@ -393,7 +438,7 @@ int run_passes(heat1d_t h, int64_t nt) {
                 if (rc) return rc;
                 for (const Slab &s : h->slabs) {
                     CK(heat1d::launch_edges(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp, h->q,
-                                            heat1d::scale_of(h->r, Tp), h->comm));
+                                            heat1d::scale_of(h->r, Tp), guard_for(h, h->ops, Tp), h->comm));
                     h->launches++;
                 }
             }
@@ -466,23 +511,25 @@ int run_maybe_graph(heat1d_t h, int64_t nt) {
     return run_passes(h, nt);
 }
 
-// K6 across ranks: agree (NCCL min-reduce) that every rank's slab fits; then allocate this
+// Collective min over ranks of a local int (NCCL on the comm stream; synchronous).
+int vote_min(heat1d_t h, int mine, int *all) {
+    int *dv = nullptr;
+    CK(cudaMalloc(&dv, sizeof(int)));
+    CK(cudaMemcpy(dv, &mine, sizeof(int), cudaMemcpyHostToDevice));
+    NK(ncclAllReduce(dv, dv, 1, ncclInt32, ncclMin, h->nccl, h->comm));
+    CK(cudaMemcpyAsync(all, dv, sizeof(int), cudaMemcpyDeviceToHost, h->comm));
+    CK(cudaStreamSynchronize(h->comm));
+    CK(cudaFree(dv));
+    return HEAT1D_OK;
+}
+
+// K6 across ranks (every rank's slab fits: vote_min at create): allocate this
 // rank's mailbox and map the two neighbours' mailboxes (CUDA IPC handles all-gathered
 // over NCCL, opened with lazy peer access: remote stores travel over NVLink).
-int setup_multi_resident(heat1d_t h, bool local_fits) {
+int setup_multi_resident(heat1d_t h) {
     const int G = h->nranks;
     int *dv = nullptr;
     CK(cudaMalloc(&dv, sizeof(int)));
-    const int mine = local_fits ? 1 : 0;
-    CK(cudaMemcpy(dv, &mine, sizeof(int), cudaMemcpyHostToDevice));
-    NK(ncclAllReduce(dv, dv, 1, ncclInt32, ncclMin, h->nccl, h->comm));
-    int all = 0;
-    CK(cudaMemcpyAsync(&all, dv, sizeof(int), cudaMemcpyDeviceToHost, h->comm));
-    CK(cudaStreamSynchronize(h->comm));
-    if (!all) {
-        CK(cudaFree(dv));
-        return HEAT1D_OK;  // K2 passes + NCCL exchange
-    }
     CK(cudaMalloc(&h->mbox, heat1d::MBOX_BYTES));
     CK(heat1d::launch_mbox_init(h->mbox, h->comm));
     CK(cudaStreamSynchronize(h->comm));
@@ -498,15 +545,31 @@ int setup_multi_resident(heat1d_t h, bool local_fits) {
     CK(cudaFree(dh));
     const int left = (h->rank - 1 + G) % G, right = (h->rank + 1) % G;
     void *pl = nullptr, *pr = nullptr;
-    CK(cudaIpcOpenMemHandle(&pl, all_h[(size_t)left], cudaIpcMemLazyEnablePeerAccess));
-    h->mbox_left = static_cast<double *>(pl);
-    h->mbox_ipc_left = true;
-    if (right == left) {
-        pr = pl;
+    // every rank must map both neighbours' mailboxes, else all fall back to K2 passes with the
+    // NCCL transport (T = Tr is a valid K2 depth: Tr <= the smallest slab)
+    int ok = cudaIpcOpenMemHandle(&pl, all_h[(size_t)left], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+    h->mbox_ipc_left = ok != 0;
+    if (ok && right != left) {
+        ok = cudaIpcOpenMemHandle(&pr, all_h[(size_t)right], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+        h->mbox_ipc_right = ok != 0;
     } else {
-        CK(cudaIpcOpenMemHandle(&pr, all_h[(size_t)right], cudaIpcMemLazyEnablePeerAccess));
-        h->mbox_ipc_right = true;
+        pr = pl;
     }
+    cudaGetLastError();
+    int all_ok = 0;
+    int rc = vote_min(h, ok, &all_ok);
+    if (rc) return rc;
+    if (!all_ok) {
+        if (h->mbox_ipc_left) cudaIpcCloseMemHandle(pl);
+        if (h->mbox_ipc_right) cudaIpcCloseMemHandle(pr);
+        h->mbox_ipc_left = h->mbox_ipc_right = false;
+        CK(cudaFree(h->mbox));
+        h->mbox = nullptr;
+        CK(cudaFree(dv));
+        h->transport = HEAT1D_TRANSPORT_NCCL;
+        return HEAT1D_OK;
+    }
+    h->mbox_left = static_cast<double *>(pl);
     h->mbox_right = static_cast<double *>(pr);
     // barrier: every rank's mailbox is zeroed and mapped before any rank's first K6 launch
     CK(cudaDeviceSynchronize());
@@ -681,13 +744,7 @@ int heat1d_plan_exchange(int64_t nx, int64_t np, int32_t nranks, int32_t rank, i
     int rc = partition(nx, np, nranks, rank, &first, &count);
     if (rc) return rc;
     if (T > min_slab(nx, np, nranks)) return HEAT1D_EINVAL;
-    plan->left = (rank - 1 + nranks) % nranks;
-    plan->right = (rank + 1) % nranks;
-    plan->send_right_off = count - T;
-    plan->send_left_off = 0;
-    plan->recv_left_off = -(int64_t)T;
-    plan->recv_right_off = count;
-    plan->cells = T;
+    make_plan(count, T, rank, nranks, plan);
     return HEAT1D_OK;
 }
 
@@ -791,7 +848,14 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     h->use_graphs = o.use_graphs != 0 && o.nranks == 1 && o.transport != HEAT1D_TRANSPORT_P2P;
     h->window_cells = o.window_cells;
     h->transport = o.transport;  // (P2P pass arguments carry exchange indices: never replayed)
-    h->ops = (o.mode == HEAT1D_MODE_FAST || is_pow2(r) || r == 0.0) ? 3 : 4;
+    // Matched mode: the 3-op form for r = 2^-j (j <= 7) or 0, else the 4-op form; both guarded
+    // per block of steps, falling back to the literal sequence where they could differ from it
+    // (stencil.cuh; DESIGN.md c3).  j <= 7 keeps the guard's bottom bound 2^(j T_MAX - 1022)
+    // far below the values a ring holds.
+    int r_exp = 0;
+    if (r > 0.0) std::frexp(r, &r_exp);
+    const bool pow2_ok = r == 0.0 || (is_pow2(r) && 1 - r_exp <= 7);
+    h->ops = (o.mode == HEAT1D_MODE_FAST || pow2_ok) ? 3 : 4;
     // r == 0: fma(0, t, b) == b + 0*t == b for finite t (identity either way)
     // Fast mode works on the scaled state v = u / r^t (stencil.cuh, DESIGN.md §3 c21): 1 DP op per
     // update at r = 1/2, 2 for 1/256 <= r < 1/2 (the state grows by at most r^-T <= 2^512 within a
@@ -827,8 +891,47 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     }
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
 
-    // T and the kernel family.  K6 (whole solve on chip) for one slab on one rank
-    // when the ring fits; otherwise K2 passes.
+    // Streams, and (several ranks) the NCCL communicator -- first, so that every decision
+    // below that depends on a rank's own slab is agreed collectively before anything is
+    // sized by it (T, pad, the kernel family).
+    if (o.stream) {
+        h->stream = static_cast<cudaStream_t>(o.stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            set_error(nullptr, HEAT1D_ECUDA, "stream create");
+            return bail(HEAT1D_ECUDA);
+        }
+        h->own_stream = true;
+    }
+    if (G > 1) {
+        if (o.comm_stream) {
+            h->comm = static_cast<cudaStream_t>(o.comm_stream);
+        } else {
+            if (cudaStreamCreateWithFlags(&h->comm, cudaStreamNonBlocking) != cudaSuccess) {
+                set_error(nullptr, HEAT1D_ECUDA, "stream create");
+                return bail(HEAT1D_ECUDA);
+            }
+            h->own_comm = true;
+        }
+        if (cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming) != cudaSuccess) {
+            set_error(nullptr, HEAT1D_ECUDA, "event create");
+            return bail(HEAT1D_ECUDA);
+        }
+    }
+    if (o.nranks > 1) {
+        ncclUniqueId id;
+        memcpy(&id, o.nccl_id, sizeof id);
+        ncclResult_t ne = ncclCommInitRank(&h->nccl, o.nranks, id, o.rank);
+        if (ne != ncclSuccess) {
+            h->nccl = nullptr;
+            set_error(nullptr, HEAT1D_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(ne));
+            return bail(HEAT1D_ENCCL);
+        }
+    }
+
+    // T and the kernel family.  K2 passes: T from opts or auto_T, clamped to
+    // the smallest slab (and half of it for the P2P edge strips) -- the same on every rank.
     int T = o.T > 0 ? o.T : auto_T(h->ops_fast ? h->ops_fast : h->ops);
     if (o.kernel == HEAT1D_KERNEL_NAIVE) T = 1;
     if (T > mslab) T = (int)mslab;  // a slab must hold its own halo
@@ -840,8 +943,10 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
         else if (T > mslab / 2)
             T = (int)(mslab / 2);  // K3p's two strips must not overlap
     }
-    // K6 across ranks (one slab per rank): every rank must agree, decided after NCCL init
-    bool res_multi_local = false;
+    // K6 (whole solve on chip) for one slab per rank when every rank's slab fits; its period
+    // Tr is again the same on every rank, but "fits" depends on the rank's own slab: the ranks
+    // vote (NCCL min-reduce) and all take the same family, T and pad.
+    bool res_multi = false;
     const bool res_ok = ((G == 1) || (o.nranks > 1 && o.virtual_slabs == 1)) && o.kernel == HEAT1D_KERNEL_AUTO &&
                         o.resident != 0 && o.window_cells == 0;
     if (res_ok) {
@@ -856,26 +961,33 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
         if (Tr > mslab) Tr = (int)mslab;
         int coop = 0;
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
-        const bool fits = coop && n0 <= heat1d::resident_capacity(Tr, h->num_sms) && n0 >= Tr &&
-                          heat1d::resident_fits(h->ops, n0, Tr, h->num_sms, G > 1) &&
-                          (!h->ops_fast || heat1d::resident_fits(h->ops_fast, n0, Tr, h->num_sms, G > 1));
+        bool fits = coop && n0 <= heat1d::resident_capacity(Tr, h->num_sms) && n0 >= Tr &&
+                    heat1d::resident_fits(h->ops, n0, Tr, h->num_sms, G > 1) &&
+                    (!h->ops_fast || heat1d::resident_fits(h->ops_fast, n0, Tr, h->num_sms, G > 1));
         cudaGetLastError();
-        if (fits && G > 1) {
-            res_multi_local = true;  // tentatively: T = Tr; agreed on below
+        if (o.nranks > 1) {
+            int all = 0;
+            int rc = vote_min(h, fits ? 1 : 0, &all);
+            if (rc) {
+                set_error(nullptr, rc, "resident vote: %s", h->last_error.c_str());
+                return bail(rc);
+            }
+            fits = all != 0;
+        }
+        if (fits) {
             T = Tr;
-        } else if (fits) {
-            h->resident = true;
-            T = Tr;
+            if (G > 1)
+                res_multi = true;  // mailboxes mapped below
+            else
+                h->resident = true;
         } else if (o.resident == 1) {
-            set_error(nullptr, HEAT1D_EUNSUPPORTED, "ring of %lld cells does not fit the resident kernel",
-                      (long long)n0);
-            delete h;
-            return HEAT1D_EUNSUPPORTED;
+            set_error(nullptr, HEAT1D_EUNSUPPORTED, "a slab of %lld cells does not fit the resident kernel%s",
+                      (long long)n0, o.nranks > 1 ? " (on some rank)" : "");
+            return bail(HEAT1D_EUNSUPPORTED);
         }
     } else if (o.resident == 1) {
         set_error(nullptr, HEAT1D_EUNSUPPORTED, "resident kernel needs one slab on one rank");
-        delete h;
-        return HEAT1D_EUNSUPPORTED;
+        return bail(HEAT1D_EUNSUPPORTED);
     }
     h->T = T;
     h->pad = pad_for(T);
@@ -921,40 +1033,7 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
         p += 2 * len;
     }
 
-    if (o.stream) {
-        h->stream = static_cast<cudaStream_t>(o.stream);
-    } else {
-        if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
-            set_error(nullptr, HEAT1D_ECUDA, "stream create");
-            return bail(HEAT1D_ECUDA);
-        }
-        h->own_stream = true;
-    }
-    if (G > 1) {
-        if (o.comm_stream) {
-            h->comm = static_cast<cudaStream_t>(o.comm_stream);
-        } else {
-            if (cudaStreamCreateWithFlags(&h->comm, cudaStreamNonBlocking) != cudaSuccess) {
-                set_error(nullptr, HEAT1D_ECUDA, "stream create");
-                return bail(HEAT1D_ECUDA);
-            }
-            h->own_comm = true;
-        }
-        if (cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming) != cudaSuccess) {
-            set_error(nullptr, HEAT1D_ECUDA, "event create");
-            return bail(HEAT1D_ECUDA);
-        }
-    }
     if (o.nranks > 1) {
-        ncclUniqueId id;
-        memcpy(&id, o.nccl_id, sizeof id);
-        ncclResult_t ne = ncclCommInitRank(&h->nccl, o.nranks, id, o.rank);
-        if (ne != ncclSuccess) {
-            h->nccl = nullptr;
-            set_error(nullptr, HEAT1D_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(ne));
-            return bail(HEAT1D_ENCCL);
-        }
         // one warm-up exchange (contents irrelevant: the first pass's exchange overwrites the
         // pads) so NCCL's p2p connections exist before the first timed pass and a broken
         // transport fails here, at create
@@ -964,14 +1043,14 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
             set_error(nullptr, rc, "warm-up halo exchange failed: %s", h->last_error.c_str());
             return bail(rc);
         }
-        if (res_ok) {
-            rc = setup_multi_resident(h, res_multi_local);
+        if (res_multi) {
+            rc = setup_multi_resident(h);
             if (rc) {
                 set_error(nullptr, rc, "multi-rank resident setup: %s", h->last_error.c_str());
                 return bail(rc);
             }
-            if (!h->resident && o.resident == 1) {
-                set_error(nullptr, HEAT1D_EUNSUPPORTED, "a rank's slab does not fit the resident kernel");
+            if (!h->resident && o.resident == 1) {  // (agreed: every rank sees the same outcome)
+                set_error(nullptr, HEAT1D_EUNSUPPORTED, "resident kernel across ranks needs peer access");
                 return bail(HEAT1D_EUNSUPPORTED);
             }
         }
@@ -1194,7 +1273,7 @@ int solve_window(heat1d_t h, int ops, double *X, double *Y, int64_t Lw, int64_t 
         const int Tp = (int)std::min<int64_t>(h->T, nt - done);
         int grid = 0;
         CK(heat1d::launch_pass(h->geom, ops, a, b, Lw, Tp, done + Tp, Lw - done - Tp, 0, q,
-                               heat1d::scale_of(h->r, Tp), h->num_sms, h->stream, &grid));
+                               heat1d::scale_of(h->r, Tp), guard_for(h, ops, Tp), h->num_sms, h->stream, &grid));
         h->launches++;
         std::swap(a, b);
         done += Tp;
@@ -1236,6 +1315,8 @@ bool fast_range_ok(heat1d_t h, unsigned long long bits) {
 bool stream_plan(heat1d_t h, int64_t nt, int64_t *C, int64_t *L, int64_t *half) {
     if (h->slabs.size() > 1 || h->resident || h->kernel == HEAT1D_KERNEL_NAIVE || nt < 1) return false;
     const int64_t n = h->slabs[0].count;
+    // a window's halos come from at most one neighbour slab (or one wrap) per side
+    if (nt > n) return false;
     *half = h->buf_len / kWinSlots / 32 * 32;  // window slots per ping-pong buffer
     const int64_t lw_max = *half - 2 * h->pad;
     const int64_t lmax = lw_max - 2 * nt;
@@ -1346,8 +1427,9 @@ int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, d
     }
     if (!plan) {  // the plain sequence
         if (h->window_cells)
-            return set_error(h, HEAT1D_EUNSUPPORTED, "window of %lld cells too small for nt=%lld (needs >= 18 nt)",
-                             (long long)h->window_cells, (long long)nt);
+            return set_error(h, HEAT1D_EUNSUPPORTED,
+                             "streaming needs window_cells >= 18 nt and nt <= ring cells (window %lld, nt %lld, N %lld)",
+                             (long long)h->window_cells, (long long)nt, (long long)count);
         rc = heat1d_set_initial(h, u0, count);
         if (!rc) rc = heat1d_run(h, nt);
         if (!rc) rc = heat1d_get(h, out, count);
@@ -1357,19 +1439,19 @@ int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, d
         return solve_windows(h, u0, u0 + (count - nt), u0, nt, out, C, L, half);
     // several ranks: ONE exchange of nt-deep halos (the light cone of the whole solve), then
     // every rank streams its windows with no further communication
-    double *hb = nullptr;  // [send first nt | send last nt | recv left | recv right]
-    CK(cudaMalloc(&hb, (size_t)4 * nt * sizeof(double)));
-    CK(cudaMemcpyAsync(hb, u0, (size_t)nt * 8, cudaMemcpyDefault, h->comm));
-    CK(cudaMemcpyAsync(hb + nt, u0 + (count - nt), (size_t)nt * 8, cudaMemcpyDefault, h->comm));
-    const int left = (h->rank - 1 + h->nranks) % h->nranks, right = (h->rank + 1) % h->nranks;
-    NK(ncclGroupStart());
-    NK(ncclSend(hb + nt, (size_t)nt, ncclDouble, right, h->nccl, h->comm));
-    NK(ncclSend(hb, (size_t)nt, ncclDouble, left, h->nccl, h->comm));
-    NK(ncclRecv(hb + 2 * nt, (size_t)nt, ncclDouble, left, h->nccl, h->comm));
-    NK(ncclRecv(hb + 3 * nt, (size_t)nt, ncclDouble, right, h->nccl, h->comm));
-    NK(ncclGroupEnd());
+    // staging in device memory (u0 is a host array): hb = [left halo (nt) | the slab's first nt
+    // cells | gap | its last nt cells | right halo (nt)] laid out so that the plan's offsets
+    // apply unchanged with "cell 0" at hb + nt and a virtual slab of 3 nt cells
+    heat1d_exchange_plan pl;
+    make_plan(3 * nt, nt, h->rank, h->nranks, &pl);
+    double *hb = nullptr;
+    CK(cudaMalloc(&hb, (size_t)5 * nt * sizeof(double)));
+    double *c0 = hb + nt;
+    CK(cudaMemcpyAsync(c0 + pl.send_left_off, u0, (size_t)nt * 8, cudaMemcpyDefault, h->comm));
+    CK(cudaMemcpyAsync(c0 + pl.send_right_off, u0 + (count - nt), (size_t)nt * 8, cudaMemcpyDefault, h->comm));
+    NK(issue_plan(pl, c0, c0, h->nccl, h->comm));
     CK(cudaStreamSynchronize(h->comm));
-    rc = solve_windows(h, u0, hb + 2 * nt, hb + 3 * nt, nt, out, C, L, half);
+    rc = solve_windows(h, u0, c0 + pl.recv_left_off, c0 + pl.recv_right_off, nt, out, C, L, half);
     if (rc) {
         cudaFree(hb);
         return rc;

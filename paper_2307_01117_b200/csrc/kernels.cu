@@ -1,9 +1,8 @@
 // kernels.cu -- sm_100a kernels of libheat1d.
 //
 //   K2 k2p_pass     T fused Jacobi steps of Eq. 2 per HBM pass (the hot kernel): TMA
-//                   producer warp, register-resident warp spans, kinds 2-4 (kind 4 =
-//                   default: 16-deep ghost exchange between the warps of a CTA);
-//                   k2_pass / k2w_pass are the earlier kinds 0 / 1, kept selectable
+//                   producer warp, register-resident warp spans trading 16-deep (kind 4,
+//                   default) or 8-deep (kind 3, small slabs) ghost zones between warps
 //   K1 k1_naive     one step per launch, modular indexing (T = 1 baseline)
 //   K3 k3_edges     the two T-wide edge strips of a slab once its ghosts arrived
 //   K3p k3_edges_put  K3 fused with the halo put into the neighbours' pads (P2P
@@ -59,11 +58,6 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
     return ok != 0;
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    while (!mbar_try_wait(bar, parity)) {
-    }
 }
 
 // Producer-side wait: the tile it waits for takes ~10 us of compute, so poll with a
@@ -146,10 +140,8 @@ __device__ __forceinline__ void warp_step(const double (&u)[V], double (&v)[V], 
     v[V - 1] = eq2<OPS>(u[V - 2], u[V - 1], R, r);
 }
 
-// T steps in registers, ping-pong between u and a scratch array (no moves
-// inside the loop); the result is left in u.
-// N (even, compile time) steps fully unrolled: the sub-periods of the exchanging
-// pass kinds, with no loop control between steps.
+// N (even, compile time) steps fully unrolled: the sub-periods of the 1-op form, with
+// no loop control between steps; the result is left in u.
 template <int V, int OPS, int N>
 __device__ __forceinline__ void warp_steps_fixed(double (&u)[V], double r) {
     static_assert(N % 2 == 0, "even step count keeps the result in u");
@@ -161,10 +153,10 @@ __device__ __forceinline__ void warp_steps_fixed(double (&u)[V], double r) {
     }
 }
 
-// Scaled variants (OPS <= 2) end the pass with u = v * r^T (`scale`, stencil.cuh),
-// unless RESCALE is false (a pass split into sub-periods rescales once at its end).
-template <int V, int OPS, bool RESCALE = true>
-__device__ __forceinline__ void warp_steps(double (&u)[V], int T, double r, double scale) {
+// T steps in registers, ping-pong between u and a scratch array (no moves
+// inside the loop); the result is left in u.
+template <int V, int OPS>
+__device__ __forceinline__ void warp_steps(double (&u)[V], int T, double r) {
     double v[V];
     int s = 0;
     for (; s + 2 <= T; s += 2) {
@@ -176,259 +168,154 @@ __device__ __forceinline__ void warp_steps(double (&u)[V], int T, double r, doub
 #pragma unroll
         for (int j = 0; j < V; ++j) u[j] = v[j];
     }
-    if constexpr (ops_scaled(OPS) && RESCALE) {
-#pragma unroll
-        for (int j = 0; j < V; ++j) u[j] = __dmul_rn(u[j], scale);
-    }
+}
+
+// Named barrier 1 among the compute warps, AND-reducing a predicate (bar.red.and).
+template <int NTHREADS>
+__device__ __forceinline__ bool bar1_and(bool ok) {
+    uint32_t res;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t"
+        "setp.ne.u32 q, %1, 0;\n\t"
+        "bar.red.and.pred p, 1, %2, q;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(res)
+        : "r"((uint32_t)ok), "n"(NTHREADS)
+        : "memory");
+    return res != 0;
 }
 
 // ------------------------------------------------------------------ K2
 //
-// Persistent CTAs walk output tiles of W = NW*(32V - 2T) cells, round robin.
-// Tile [x0, x1) needs inputs [x0-T, x1+T): one TMA bulk copy (aligned down/up
-// to 16 B) lands them in an S-stage shared-memory ring (mbarrier complete_tx).
-// Warp w takes the 32V-cell span starting at w*(32V-2T) of the tile input;
-// lane l holds V consecutive cells in registers.  Each of the T steps fetches
-// the two inter-lane neighbours with shuffles; the warp's outermost cells go
-// stale by one cell per step (a per-warp trapezoid), so after T steps the
-// warp's 32V-2T central cells are exact.  Those are written back in place,
-// and one bulk copy stores the tile.  V odd makes the 64-bit shared accesses
-// of a half-warp hit 16 distinct bank pairs.
-template <int V, int NW, int S, int OPS>
-__global__ void __launch_bounds__(NW * 32)
-k2_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t out_lo,
-        int64_t out_hi, int wrapT, double r, double scale, int64_t ntiles, uint32_t stage_doubles) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);
-    double *stages = reinterpret_cast<double *>(smem_raw + 128);
+// k2p_pass: persistent CTAs of NW compute warps plus one TMA producer warp walk
+// output tiles, round robin.  Tile [x0, x1) needs inputs [x0-T, x1+T): the
+// producer's 1D bulk copy (aligned down/up to 16 B; SASS UBLKCP) lands them in an
+// S-stage shared-memory ring (mbarrier complete_tx); once the compute warps
+// signal done[s] it bulk-stores the results and refills the stage.
+//
+// Compute warp w holds tile-input cells [w(32V-2KX), w(32V-2KX)+32V), V per lane
+// in registers; every step fetches the two inter-lane neighbours with shuffles.
+// Every KX steps the warps trade KX-deep ghost zones through shared memory
+// (kind 3: KX = 8, kind 4: KX = 16) -- PAPER.md:73's ghost exchange between
+// neighbouring segments, at depth KX, between warps: after KX steps a warp's KX
+// outermost cells on an inner side are stale and are refreshed from the
+// neighbour warp's first/last KX owned cells (lane 0 / lane 31 registers; one
+// named barrier per exchange, slots double-buffered by parity).  Only the CTA's
+// two outer sides keep the T-deep trapezoid, so the redundant work is
+// (2T + 2KX(NW-1))/(NW 32V).  V odd makes the 64-bit shared accesses of a
+// half-warp hit 16 distinct bank pairs.
+//
+// Guarded variants (OPS 4, 3; stencil.cuh): every compute warp checks the input
+// cells of its span (GuardAcc, 5 integer instructions per cell and tile) and the
+// verdicts are AND-reduced in the first barrier the compute warps pass anyway; a tile
+// that fails is redone -- by every warp, the decision is CTA-uniform -- with the
+// literal 5-op sequence.  (Scanning the stages in the idle producer warp instead cost
+// 5 % at C4: it loads one SM sub-partition unevenly.)
 
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform for the compiler
-    const int OW = 32 * V - 2 * T;
-    const int64_t W = (int64_t)NW * OW;
-
-    const uint64_t pol_in = policy_evict_first();
-
-    if (tid == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    const int64_t stride = gridDim.x;
-
-    auto issue_load = [&](int64_t tile, int s) {
-        const int64_t x0 = out_lo + tile * W;
-        const int64_t x1 = min(x0 + W, out_hi);
-        const int64_t lo = x0 - T;
-        const int64_t ld_lo = lo - (lo & 1);
-        int64_t ld_hi = x1 + T;
-        ld_hi += (ld_hi & 1);
-        const uint32_t bytes = (uint32_t)((ld_hi - ld_lo) * 8);
-        mbar_arrive_expect_tx(&full[s], bytes);
-        bulk_g2s(stages + (size_t)s * stage_doubles, A + ld_lo, bytes, &full[s], pol_in);
-    };
-
-    if (tid == 0) {
-        for (int i = 0; i < S - 1; ++i) {
-            const int64_t tile = blockIdx.x + i * stride;
-            if (tile >= ntiles) break;
-            issue_load(tile, i);
-        }
-    }
-
-    int k = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += stride, ++k) {
-        const int s = k % S;
-        const uint32_t parity = (uint32_t)((k / S) & 1);
-        double *st = stages + (size_t)s * stage_doubles;
-
-        const int64_t x0 = out_lo + tile * W;
-        const int64_t x1 = min(x0 + W, out_hi);
-        const int64_t lo = x0 - T;
-        const int sh = (int)(lo & 1);
-        const int64_t ld_lo = lo - sh;
-
-        mbar_wait(&full[s], parity);
-
-        const int base = sh + warp * OW + lane * V;
-        double u[V];
-#pragma unroll
-        for (int j = 0; j < V; ++j) u[j] = st[base + j];
-
-        __syncthreads();  // B1: every warp has its span in registers -> in-place writes are safe
-
-        warp_steps<V, OPS>(u, T, r, scale);
-
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-            const int p = lane * V + j;
-            if (p >= T && p < 32 * V - T) st[base + j] = u[j];
-        }
-        fence_proxy_async();
-        __syncthreads();  // B2: tile outputs complete in shared memory
-
-        if (tid == 0) {
-            const int64_t a = x0 + (x0 & 1);
-            const int64_t b = x1 - (x1 & 1);
-            if (b > a) bulk_s2g(B + a, st + (a - ld_lo), (uint32_t)((b - a) * 8));
-            bulk_commit();  // one group per tile, possibly empty
-            const int64_t nxt = tile + (int64_t)(S - 1) * stride;
-            if (nxt < ntiles) {
-                bulk_wait_read<1>();  // the store that last used stage (k+S-1)%S has read it
-                fence_proxy_async();
-                issue_load(nxt, (k + S - 1) % S);
+// The steps of a tile.  The first barrier among the compute warps (the first ghost
+// exchange, or for T <= KX a barrier after the steps) orders every warp's span load
+// before any warp's in-place write-back; with GUARD it also AND-reduces `ok` and the
+// function returns false on every warp if some cell failed (nothing was written back:
+// the stage still holds the tile's input).
+template <int V, int NW, int KX, int OPS, bool GUARD>
+__device__ __forceinline__ bool tile_steps(double (&u)[V], int T, double r, double scale, double *xbuf,
+                                           int warp, int lane, bool ok) {
+    int dn = 0;
+    for (int e = 0;; ++e) {
+        const int Ks = (T - dn) < KX ? (T - dn) : KX;
+        // (full unrolling pays for the 1-op form only: the 3/4-op sub-period
+        // code would outgrow the instruction cache)
+        if (OPS == 1 && Ks == KX)
+            warp_steps_fixed<V, OPS, KX>(u, r);
+        else
+            warp_steps<V, OPS>(u, Ks, r);  // (scaled forms: rescale below, once per pass)
+        dn += Ks;
+        if (dn >= T) {
+            if (e == 0) {  // no exchange happened: the load-before-write-back barrier
+                if constexpr (GUARD) {
+                    if (!__shfl_sync(0xffffffffu, (int)bar1_and<NW * 32>(ok), 0)) return false;
+                } else {
+                    asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+                }
             }
-            if (x0 & 1) B[x0] = st[x0 - ld_lo];
+            break;
         }
-        if (tid == 1 && (x1 & 1) && x1 - 1 >= x0) B[x1 - 1] = st[x1 - 1 - ld_lo];
-        for (int j = tid; j < wrapT; j += blockDim.x) {
-            if (j >= x0 && j < x1) B[n + j] = st[j - ld_lo];
-            const int64_t c = n - wrapT + j;
-            if (c >= x0 && c < x1) B[j - wrapT] = st[c - ld_lo];
+        double *X = xbuf + (size_t)(e & 1) * (NW * 2 * KX);
+        if (lane == 0 && warp > 0) {
+#pragma unroll
+            for (int i = 0; i < KX; ++i) X[(warp * 2 + 0) * KX + i] = u[KX + i];
+        }
+        if (lane == 31 && warp < NW - 1) {
+#pragma unroll
+            for (int i = 0; i < KX; ++i) X[(warp * 2 + 1) * KX + i] = u[V - 2 * KX + i];
+        }
+        if (GUARD && e == 0) {
+            // (the reduction is CTA-uniform; the broadcast lets ptxas prove it warp-uniform,
+            // or the shuffles of the step loops become WARPSYNC-collective sequences)
+            if (!__shfl_sync(0xffffffffu, (int)bar1_and<NW * 32>(ok), 0)) return false;
+        } else {
+            asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+        }
+        if (lane == 0 && warp > 0) {
+#pragma unroll
+            for (int i = 0; i < KX; ++i) u[i] = X[((warp - 1) * 2 + 1) * KX + i];
+        }
+        if (lane == 31 && warp < NW - 1) {
+#pragma unroll
+            for (int i = 0; i < KX; ++i) u[V - KX + i] = X[((warp + 1) * 2 + 0) * KX + i];
         }
     }
-    if (tid == 0) bulk_wait<0>();
+    if constexpr (ops_scaled(OPS)) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) u[j] = __dmul_rn(u[j], scale);
+    }
+    return true;
 }
 
-// ------------------------------------------------------------------ K2 (warp-autonomous)
-//
-// Same arithmetic and the same per-warp trapezoid as k2_pass, but every warp
-// owns an S-slot TMA ring of 32V-cell spans and its own mbarriers: lane 0
-// issues the bulk load of the span [x0-T, x0+OW+T) and, after the warp has
-// written its OW = 32V-2T exact outputs back into the slot, the bulk store.
-// No CTA-wide barrier exists, so warps never wait for each other.  Adjacent
-// global warps take adjacent spans, so the 2T-cell overlaps hit in L2.
-template <int V, int NW, int S, int OPS>
-__global__ void __launch_bounds__(NW * 32)
-k2w_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t out_lo,
-         int64_t out_hi, int wrapT, double r, double scale, int64_t nspans, uint32_t slot_doubles) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    constexpr int BAR_BYTES = ((NW * S * 8 + 127) / 128) * 128;
-    const int lane = threadIdx.x & 31;
-    const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);  // warp-uniform for the compiler
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw) + warp * S;
-    double *slots = reinterpret_cast<double *>(smem_raw + BAR_BYTES) + (size_t)warp * S * slot_doubles;
-
-    const int OW = 32 * V - 2 * T;
-    const int64_t stride = (int64_t)gridDim.x * NW;
-    const int64_t first = (int64_t)blockIdx.x * NW + warp;
-    const uint64_t pol_in = policy_evict_first();
-
-    if (lane == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-        fence_mbar_init();
-    }
-    __syncwarp();
-
-    auto issue_load = [&](int64_t sp, int s) {
-        const int64_t x0 = out_lo + sp * OW;
-        const int64_t x1 = min(x0 + OW, out_hi);
-        const int64_t lo = x0 - T;
-        const int64_t ld_lo = lo - (lo & 1);
-        int64_t ld_hi = x1 + T;
-        ld_hi += (ld_hi & 1);
-        const uint32_t bytes = (uint32_t)((ld_hi - ld_lo) * 8);
-        mbar_arrive_expect_tx(&bars[s], bytes);
-        bulk_g2s(slots + (size_t)s * slot_doubles, A + ld_lo, bytes, &bars[s], pol_in);
-    };
-
-    if (lane == 0) {
-        for (int i = 0; i < S - 1; ++i) {
-            const int64_t sp = first + i * stride;
-            if (sp >= nspans) break;
-            issue_load(sp, i);
-        }
-    }
-
-    int k = 0;
-    for (int64_t sp = first; sp < nspans; sp += stride, ++k) {
-        const int s = k % S;
-        const uint32_t parity = (uint32_t)((k / S) & 1);
-        double *st = slots + (size_t)s * slot_doubles;
-        const int64_t x0 = out_lo + sp * OW;
-        const int64_t x1 = min(x0 + OW, out_hi);
-        const int64_t lo = x0 - T;
-        const int sh = (int)(lo & 1);
-        const int64_t ld_lo = lo - sh;
-
-        mbar_wait(&bars[s], parity);
-        const int base = sh + lane * V;
-        double u[V];
+// In-place write-back of a warp's owned cells (inner sides exclude the KX ghost zone,
+// the CTA's outer sides the T-deep one).
+template <int V, int NW, int KX>
+__device__ __forceinline__ void write_back(const double (&u)[V], double *st, int base, int T, int warp, int lane) {
+    const int lo = warp == 0 ? T : KX;
+    const int hi = warp == NW - 1 ? 32 * V - T : 32 * V - KX;
 #pragma unroll
-        for (int j = 0; j < V; ++j) u[j] = st[base + j];
-
-        warp_steps<V, OPS>(u, T, r, scale);
-
-        // each lane rewrites only its own cells: no intra-warp WAR hazard
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-            const int p = lane * V + j;
-            if (p >= T && p < 32 * V - T) st[base + j] = u[j];
-        }
-        fence_proxy_async();
-        __syncwarp();
-
-        if (lane == 0) {
-            const int64_t a = x0 + (x0 & 1);
-            const int64_t b = x1 - (x1 & 1);
-            if (b > a) bulk_s2g(B + a, st + (a - ld_lo), (uint32_t)((b - a) * 8));
-            bulk_commit();
-            const int64_t nxt = sp + (int64_t)(S - 1) * stride;
-            if (nxt < nspans) {
-                bulk_wait_read<1>();
-                fence_proxy_async();
-                issue_load(nxt, (k + S - 1) % S);
-            }
-            if (x0 & 1) B[x0] = st[x0 - ld_lo];
-        }
-        if (lane == 1 && (x1 & 1) && x1 - 1 >= x0) B[x1 - 1] = st[x1 - 1 - ld_lo];
-        for (int j = lane; j < wrapT; j += 32) {
-            if (j >= x0 && j < x1) B[n + j] = st[j - ld_lo];
-            const int64_t c = n - wrapT + j;
-            if (c >= x0 && c < x1) B[j - wrapT] = st[c - ld_lo];
-        }
+    for (int j = 0; j < V; ++j) {
+        const int p = lane * V + j;
+        if (p >= lo && p < hi) st[base + j] = u[j];
     }
-    if (lane == 0) bulk_wait<0>();
 }
 
-// ------------------------------------------------------------------ K2 (warp-specialised)
-//
-// k2_pass with a dedicated producer warp: warps 0..NW-1 compute, warp NW owns
-// all TMA traffic.
-//
-// KX > 0 (kind 3): the compute warps of a CTA trade K-deep ghost zones through
-// shared memory every KX steps instead of each carrying a T-deep trapezoid --
-// PAPER.md:73's ghost exchange between neighbouring segments, at depth KX,
-// between warps.  Warp w holds tile-input cells [w(32V-2KX), w(32V-2KX)+32V);
-// after KX steps its KX outermost cells on an inner side are stale, and are
-// refreshed from the neighbour warp's first/last KX owned cells (lane 0 /
-// lane 31 registers; one named barrier per exchange, slots double-buffered by
-// parity).  Only the CTA's two outer sides keep the T-deep trapezoid, so the
-// redundant work falls from 2T/(32V) per warp to (2T + 2KX(NW-1))/(NW 32V).  The producer refills a stage as soon as the bulk store of
-// its previous tile has read it out, so S-1 loads are in flight while the
-// compute warps work; compute warps never wait for stores, and their only
-// CTA-level sync is a named barrier (B1) among themselves before the in-place
-// write-back.  Per stage: full[s] (TMA complete_tx) and done[s] (NW arrivals).
-template <int V, int NW, int S, int OPS, int KX = 0>
-__global__ void __launch_bounds__((NW + 1) * 32)
+// The guard's fallback (rare): a tile with the literal 5-op sequence.  Out of line, so
+// its registers do not add to the hot path's.
+template <int V, int NW, int KX>
+__device__ __noinline__ void tile_literal(double *st, int base, int T, double r, double *xbuf, int warp, int lane) {
+    double u[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) u[j] = st[base + j];
+    tile_steps<V, NW, KX, 5, false>(u, T, r, 1.0, xbuf, warp, lane, true);
+    write_back<V, NW, KX>(u, st, base, T, warp, lane);
+}
+
+// Register target: the occupancy choose_geom plans for (2 CTAs/SM; 4 for V <= 17 tiles).
+// Without it ptxas sizes the kernel for the guard's out-of-line fallback as well.
+template <int V, int NW, int S, int OPS, int KX>
+__global__ void __launch_bounds__((NW + 1) * 32, V <= 17 ? 4 : 2)
 k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t out_lo,
-         int64_t out_hi, int wrapT, double r, double scale, int64_t ntiles, uint32_t stage_doubles) {
+         int64_t out_hi, int wrapT, double r, double scale, int64_t ntiles, uint32_t stage_doubles,
+         Guard guard) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);
-    uint64_t *done = full + S;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);  // TMA landed
+    uint64_t *done = full + S;                                 // compute warps finished
     double *stages = reinterpret_cast<double *>(smem_raw + 128);
+    constexpr bool GUARD = ops_guarded(OPS);
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform for the compiler
-    // KX == 0: warp spans of 32V overlapping by 2T; KX > 0: spans overlapping by 2KX
-    const int SW = KX > 0 ? 32 * V - 2 * KX : 32 * V - 2 * T;  // span stride
-    const int OW = 32 * V - 2 * T;
-    const int64_t W = KX > 0 ? (int64_t)NW * 32 * V - 2 * KX * (NW - 1) - 2 * T : (int64_t)NW * OW;
+    const int SW = 32 * V - 2 * KX;                            // span stride
+    const int64_t W = (int64_t)NW * 32 * V - 2 * KX * (NW - 1) - 2 * T;
     const int64_t stride = gridDim.x;
-    double *xbuf = stages + (size_t)S * stage_doubles;  // KX > 0: [2 parities][NW][2 sides][KX]
+    double *xbuf = stages + (size_t)S * stage_doubles;  // [2 parities][NW][2 sides][KX]
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
@@ -442,13 +329,16 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
     if (warp == NW) {
         // ---------------- producer warp
         const uint64_t pol_in = policy_evict_first();
+        auto span_of = [&](int64_t tile, int64_t *x0, int64_t *x1, int64_t *ld_lo, int64_t *ld_hi) {
+            *x0 = out_lo + tile * W;
+            *x1 = min(*x0 + W, out_hi);
+            const int64_t lo = *x0 - T;
+            *ld_lo = lo - (lo & 1);
+            *ld_hi = *x1 + T + ((*x1 + T) & 1);
+        };
         auto issue_load = [&](int64_t tile, int s) {
-            const int64_t x0 = out_lo + tile * W;
-            const int64_t x1 = min(x0 + W, out_hi);
-            const int64_t lo = x0 - T;
-            const int64_t ld_lo = lo - (lo & 1);
-            int64_t ld_hi = x1 + T;
-            ld_hi += (ld_hi & 1);
+            int64_t x0, x1, ld_lo, ld_hi;
+            span_of(tile, &x0, &x1, &ld_lo, &ld_hi);
             const uint32_t bytes = (uint32_t)((ld_hi - ld_lo) * 8);
             mbar_arrive_expect_tx(&full[s], bytes);
             bulk_g2s(stages + (size_t)s * stage_doubles, A + ld_lo, bytes, &full[s], pol_in);
@@ -464,10 +354,8 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += stride, ++k) {
             const int s = k % S;
             double *st = stages + (size_t)s * stage_doubles;
-            const int64_t x0 = out_lo + tile * W;
-            const int64_t x1 = min(x0 + W, out_hi);
-            const int64_t lo = x0 - T;
-            const int64_t ld_lo = lo - (lo & 1);
+            int64_t x0, x1, ld_lo, ld_hi;
+            span_of(tile, &x0, &x1, &ld_lo, &ld_hi);
             mbar_wait_backoff(&done[s], (uint32_t)((k / S) & 1));
             // scalar leftovers: an odd first/last cell and the periodic self-halo
             if (lane == 0 && (x0 & 1)) B[x0] = st[x0 - ld_lo];
@@ -500,66 +388,26 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
     int k = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += stride, ++k) {
         const int s = k % S;
+        const uint32_t par = (uint32_t)((k / S) & 1);
         double *st = stages + (size_t)s * stage_doubles;
         const int64_t x0 = out_lo + tile * W;
         const int sh = (int)((x0 - T) & 1);
-        mbar_wait_sleep(&full[s], (uint32_t)((k / S) & 1));
+        mbar_wait_sleep(&full[s], par);
         const int base = sh + warp * SW + lane * V;
         double u[V];
 #pragma unroll
         for (int j = 0; j < V; ++j) u[j] = st[base + j];
-        asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");  // B1 among compute warps
-        if constexpr (KX == 0) {
-            warp_steps<V, OPS>(u, T, r, scale);
+        bool ok = true;
+        if constexpr (GUARD) {
+            GuardAcc acc;
 #pragma unroll
-            for (int j = 0; j < V; ++j) {
-                const int p = lane * V + j;
-                if (p >= T && p < 32 * V - T) st[base + j] = u[j];
-            }
-        } else {
-            int dn = 0;
-            for (int e = 0;; ++e) {
-                const int Ks = (T - dn) < KX ? (T - dn) : KX;
-                // (full unrolling pays for the 1-op form only: the 3/4-op sub-period
-                // code would outgrow the instruction cache)
-                if (OPS == 1 && Ks == KX)
-                    warp_steps_fixed<V, OPS, KX>(u, r);
-                else
-                    warp_steps<V, OPS, false>(u, Ks, r, 1.0);  // (rescale below, once per pass)
-                dn += Ks;
-                if (dn >= T) break;
-                double *X = xbuf + (size_t)(e & 1) * (NW * 2 * KX);
-                if (lane == 0 && warp > 0) {
-#pragma unroll
-                    for (int i = 0; i < KX; ++i) X[(warp * 2 + 0) * KX + i] = u[KX + i];
-                }
-                if (lane == 31 && warp < NW - 1) {
-#pragma unroll
-                    for (int i = 0; i < KX; ++i) X[(warp * 2 + 1) * KX + i] = u[V - 2 * KX + i];
-                }
-                asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
-                if (lane == 0 && warp > 0) {
-#pragma unroll
-                    for (int i = 0; i < KX; ++i) u[i] = X[((warp - 1) * 2 + 1) * KX + i];
-                }
-                if (lane == 31 && warp < NW - 1) {
-#pragma unroll
-                    for (int i = 0; i < KX; ++i) u[V - KX + i] = X[((warp + 1) * 2 + 0) * KX + i];
-                }
-            }
-            if constexpr (ops_scaled(OPS)) {
-#pragma unroll
-                for (int j = 0; j < V; ++j) u[j] = __dmul_rn(u[j], scale);
-            }
-            // owned cells: inner sides exclude the KX ghost zone, the CTA's outer sides the T-deep one
-            const int lo = warp == 0 ? T : KX;
-            const int hi = warp == NW - 1 ? 32 * V - T : 32 * V - KX;
-#pragma unroll
-            for (int j = 0; j < V; ++j) {
-                const int p = lane * V + j;
-                if (p >= lo && p < hi) st[base + j] = u[j];
-            }
+            for (int j = 0; j < V; ++j) acc.add(u[j]);
+            ok = acc.ok(guard);
         }
+        if (tile_steps<V, NW, KX, OPS, GUARD>(u, T, r, scale, xbuf, warp, lane, ok))
+            write_back<V, NW, KX>(u, st, base, T, warp, lane);
+        else
+            tile_literal<V, NW, KX>(st, base, T, r, xbuf, warp, lane);
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&done[s]);
@@ -567,71 +415,43 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
 }
 
 size_t PassGeom::smem_bytes(int T) const {
-    if (kind != 1) {
-        const int64_t in_cells = tile_out(T) + 2 * T + 2;
-        const int64_t stage = (in_cells + 15) / 16 * 16;
-        const size_t xch = (size_t)2 * NW * 2 * kx_of(kind) * sizeof(double);
-        return 128 + (size_t)S * (size_t)stage * sizeof(double) + xch;
-    }
-    const int64_t slot = (32 * (int64_t)V + 2 + 15) / 16 * 16;
-    const size_t bar = (size_t)((NW * S * 8 + 127) / 128) * 128;
-    return bar + (size_t)NW * S * (size_t)slot * sizeof(double);
+    const int64_t in_cells = tile_out(T) + 2 * T + 2;
+    const int64_t stage = (in_cells + 15) / 16 * 16;
+    const size_t xch = (size_t)2 * NW * 2 * kx_of(kind) * sizeof(double);
+    return 128 + (size_t)S * (size_t)stage * sizeof(double) + xch;
 }
 
 namespace {
 
 using PassFn = void (*)(const double *, double *, int64_t, int, int64_t, int64_t, int, double, double,
-                        int64_t, uint32_t);
+                        int64_t, uint32_t, Guard);
 
-template <int V, int NW, int S, int OPS>
-PassFn pass_fn(int kind) {
-    return kind == 0 ? &k2_pass<V, NW, S, OPS> : kind == 1 ? &k2w_pass<V, NW, S, OPS> : &k2p_pass<V, NW, S, OPS>;
-}
-
-// kinds 3 and 4 (inter-warp ghost exchange) for all four arithmetic variants
-#define HEAT1D_GEOMS_X(X) X(17, 4, 3) X(17, 8, 3) X(25, 4, 3) X(25, 8, 2) X(33, 6, 2) X(33, 4, 2) X(33, 4, 3) X(33, 8, 2) X(33, 8, 3) X(41, 4, 2) X(45, 4, 2) X(47, 4, 2) X(49, 4, 2) X(49, 8, 2) X(51, 4, 2) X(53, 4, 2) X(55, 4, 2) X(65, 4, 2)
+// (V, NW, S) instantiated for kinds 3 and 4 and all four arithmetic variants: the
+// two defaults of choose_geom (51,4,2) and (17,4,3) plus the tuning points of the
+// V sweeps.
+#define HEAT1D_GEOMS_X(X) X(17, 4, 3) X(25, 4, 3) X(33, 4, 2) X(49, 4, 2) X(51, 4, 2)
 
 template <int V, int NW, int S, int KX>
 PassFn pass_fn_x(int ops) {
-    switch (ops) {
-        case 4: return &k2p_pass<V, NW, S, 4, KX>;
-        case 3: return &k2p_pass<V, NW, S, 3, KX>;
-        case 2: return &k2p_pass<V, NW, S, 2, KX>;
-        default: return &k2p_pass<V, NW, S, 1, KX>;
+    if constexpr (V < 2 * KX) {  // the exchanged KX-cell edges must lie inside one lane
+        (void)ops;
+        return nullptr;
+    } else {
+        switch (ops) {
+            case 4: return &k2p_pass<V, NW, S, 4, KX>;
+            case 3: return &k2p_pass<V, NW, S, 3, KX>;
+            case 2: return &k2p_pass<V, NW, S, 2, KX>;
+            case 1: return &k2p_pass<V, NW, S, 1, KX>;
+            default: return nullptr;
+        }
     }
 }
 
-// (V, NW, S) instantiated for all three kernel kinds and both arithmetic variants:
-// the defaults plus the tuning points the sweeps and tests use.
-#define HEAT1D_GEOMS(X)                                                                            \
-    X(9, 4, 3) X(9, 8, 4) X(15, 8, 3) X(17, 4, 2) X(17, 4, 4) X(17, 8, 2) X(17, 8, 3) X(17, 8, 4)  \
-    X(17, 16, 2) X(21, 8, 3) X(25, 4, 3) X(25, 8, 2) X(33, 4, 2) X(33, 4, 3) X(33, 8, 2) X(33, 8, 3) \
-    X(49, 4, 3)
-
-// The scaled fast-mode variants (OPS 2, 1) exist for the producer-warp kind only,
-// at the default geometries and the tuning points of the fast-mode sweeps.
-#define HEAT1D_GEOMS_SCALED(X) X(9, 4, 3) X(17, 8, 3) X(25, 4, 3) X(33, 4, 3) X(33, 8, 3) X(49, 4, 3)
-
 PassFn lookup_pass(int V, int NW, int S, int ops, int kind) {
-    if (kind == 3 || kind == 4) {
+    if (kind != 3 && kind != 4) return nullptr;
 #define X(v, nw, s) \
     if (V == v && NW == nw && S == s) return kind == 3 ? pass_fn_x<v, nw, s, 8>(ops) : pass_fn_x<v, nw, s, 16>(ops);
-        HEAT1D_GEOMS_X(X)
-#undef X
-        return nullptr;
-    }
-    if (ops == 4 || ops == 3) {
-#define X(v, nw, s)                                                                                \
-    if (V == v && NW == nw && S == s)                                                              \
-        return ops == 4 ? pass_fn<v, nw, s, 4>(kind) : pass_fn<v, nw, s, 3>(kind);
-        HEAT1D_GEOMS(X)
-#undef X
-        return nullptr;
-    }
-    if (kind != 2) return nullptr;
-#define X(v, nw, s)                                                                                \
-    if (V == v && NW == nw && S == s) return ops == 2 ? &k2p_pass<v, nw, s, 2> : &k2p_pass<v, nw, s, 1>;
-    HEAT1D_GEOMS_SCALED(X)
+    HEAT1D_GEOMS_X(X)
 #undef X
     return nullptr;
 }
@@ -654,8 +474,8 @@ PassGeom choose_geom(int64_t n_out, int T, int num_sms, int ops) {
 }
 
 cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, int64_t n, int T,
-                        int64_t out_lo, int64_t out_hi, int wrapT, double q, double scale, int num_sms,
-                        cudaStream_t st, int *grid_out) {
+                        int64_t out_lo, int64_t out_hi, int wrapT, double q, double scale, Guard guard,
+                        int num_sms, cudaStream_t st, int *grid_out) {
     PassFn fn = lookup_pass(g.V, g.NW, g.S, ops, g.kind);
     if (!fn) return cudaErrorInvalidConfiguration;
     if (out_hi <= out_lo) {
@@ -664,13 +484,12 @@ cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, 
     }
     const int64_t W = g.tile_out(T);
     const int kx = kx_of(g.kind);
-    if (W <= 0 || (!kx && 32 * g.V - 2 * T <= 0)) return cudaErrorInvalidValue;
-    // kinds 3, 4: the outer warps' T-deep trapezoid must stay inside their span, and the
-    // exchanged KX-cell edges inside one lane
-    if (kx && (T > 32 * g.V - kx || g.V < 2 * kx)) return cudaErrorInvalidValue;
+    // the outer warps' T-deep trapezoid must stay inside their span, and the exchanged
+    // KX-cell edges inside one lane
+    if (W <= 0 || T > 32 * g.V - kx || g.V < 2 * kx) return cudaErrorInvalidValue;
     const int64_t units = (out_hi - out_lo + W - 1) / W;
     const size_t smem = g.smem_bytes(T);
-    const int64_t in_cells = (g.kind != 1 ? W : 32 * (int64_t)g.V - 2 * T) + 2 * T + 2;
+    const int64_t in_cells = W + 2 * T + 2;
     const uint32_t stage_doubles = (uint32_t)((in_cells + 15) / 16 * 16);
     // Raise the dynamic shared-memory limit once per instantiation (max over T).
     {
@@ -694,16 +513,16 @@ cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, 
     // Persistent grid: never more CTAs than can be co-resident (static round-robin
     // assignment assumes a single wave).
     int occ = 0;
-    const int threads = (g.NW + (g.kind >= 2 ? 1 : 0)) * 32;
+    const int threads = (g.NW + 1) * 32;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)fn, threads, smem) != cudaSuccess ||
         occ < 1)
         occ = 1;
     const int per_sm = g.ctas_per_sm < occ ? g.ctas_per_sm : occ;
     int64_t grid = (int64_t)num_sms * per_sm;
-    const int64_t need = g.kind != 1 ? units : (units + g.NW - 1) / g.NW;
-    if (grid > need) grid = need;
+    if (grid > units) grid = units;
     if (grid_out) *grid_out = (int)grid;
-    fn<<<(unsigned)grid, threads, smem, st>>>(A, B, n, T, out_lo, out_hi, wrapT, q, scale, units, stage_doubles);
+    fn<<<(unsigned)grid, threads, smem, st>>>(A, B, n, T, out_lo, out_hi, wrapT, q, scale, units, stage_doubles,
+                                             guard);
     return cudaGetLastError();
 }
 
@@ -722,24 +541,22 @@ __global__ void __launch_bounds__(256) k1_naive(const double *__restrict__ A, do
 cudaError_t launch_naive(int ops, const double *A, double *B, int64_t n, double r, cudaStream_t st) {
     int64_t blocks = (n + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    if (ops == 4)
-        k1_naive<4><<<(unsigned)blocks, 256, 0, st>>>(A, B, n, r);
-    else
+    if (ops == 5)
+        k1_naive<5><<<(unsigned)blocks, 256, 0, st>>>(A, B, n, r);
+    else if (ops == 3)
         k1_naive<3><<<(unsigned)blocks, 256, 0, st>>>(A, B, n, r);
+    else
+        return cudaErrorInvalidValue;
     return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ K3
 // Block 0: outputs [0,T) from A[-T, 2T); block 1: outputs [n-T, n) from A[n-2T, n+T).
 // The 3T-cell window shrinks by one cell per side per step (light cone).
+// Guarded variants (stencil.cuh) run the literal sequence if any window cell fails.
 template <int OPS>
-__global__ void __launch_bounds__(96) k3_edges(const double *__restrict__ A, double *__restrict__ B, int64_t n,
-                                               int T, double r, double scale) {
-    __shared__ double w[2][3 * 128];
-    const int64_t base = (blockIdx.x == 0) ? -(int64_t)T : n - 2 * (int64_t)T;
+__device__ __forceinline__ int strip_steps(double (*w)[3 * 128], int T, double r) {
     const int len = 3 * T;
-    for (int i = threadIdx.x; i < len; i += blockDim.x) w[0][i] = A[base + i];
-    __syncthreads();
     int cur = 0;
     for (int s = 0; s < T; ++s) {
         const int lo = s + 1, hi = len - 1 - s;  // cells valid after step s+1
@@ -748,6 +565,28 @@ __global__ void __launch_bounds__(96) k3_edges(const double *__restrict__ A, dou
         cur ^= 1;
         __syncthreads();
     }
+    return cur;
+}
+
+template <int OPS>
+__device__ __forceinline__ int strip_steps_guarded(double (*w)[3 * 128], int T, double r, Guard guard) {
+    if constexpr (ops_guarded(OPS)) {
+        GuardAcc acc;
+        for (int i = threadIdx.x; i < 3 * T; i += blockDim.x) acc.add(w[0][i]);
+        if (!__syncthreads_and(acc.ok(guard))) return strip_steps<5>(w, T, r);
+    }
+    return strip_steps<OPS>(w, T, r);
+}
+
+template <int OPS>
+__global__ void __launch_bounds__(96) k3_edges(const double *__restrict__ A, double *__restrict__ B, int64_t n,
+                                               int T, double r, double scale, Guard guard) {
+    __shared__ double w[2][3 * 128];
+    const int64_t base = (blockIdx.x == 0) ? -(int64_t)T : n - 2 * (int64_t)T;
+    const int len = 3 * T;
+    for (int i = threadIdx.x; i < len; i += blockDim.x) w[0][i] = A[base + i];
+    __syncthreads();
+    const int cur = strip_steps_guarded<OPS>(w, T, r, guard);
     for (int i = threadIdx.x; i < T; i += blockDim.x) {
         double x = w[cur][T + i];
         if constexpr (ops_scaled(OPS)) x = __dmul_rn(x, scale);
@@ -756,13 +595,13 @@ __global__ void __launch_bounds__(96) k3_edges(const double *__restrict__ A, dou
 }
 
 cudaError_t launch_edges(int ops, const double *A, double *B, int64_t n, int T, double q, double scale,
-                         cudaStream_t st) {
+                         Guard guard, cudaStream_t st) {
     if (T < 1 || T > 128) return cudaErrorInvalidValue;
     switch (ops) {
-        case 4: k3_edges<4><<<2, 96, 0, st>>>(A, B, n, T, q, scale); break;
-        case 3: k3_edges<3><<<2, 96, 0, st>>>(A, B, n, T, q, scale); break;
-        case 2: k3_edges<2><<<2, 96, 0, st>>>(A, B, n, T, q, scale); break;
-        case 1: k3_edges<1><<<2, 96, 0, st>>>(A, B, n, T, q, scale); break;
+        case 4: k3_edges<4><<<2, 96, 0, st>>>(A, B, n, T, q, scale, guard); break;
+        case 3: k3_edges<3><<<2, 96, 0, st>>>(A, B, n, T, q, scale, guard); break;
+        case 2: k3_edges<2><<<2, 96, 0, st>>>(A, B, n, T, q, scale, guard); break;
+        case 1: k3_edges<1><<<2, 96, 0, st>>>(A, B, n, T, q, scale, guard); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -789,9 +628,9 @@ __device__ __forceinline__ void st_release_sys_u32(unsigned *p, unsigned v) {
 
 template <int OPS>
 __global__ void __launch_bounds__(96) k3_edges_put(const double *__restrict__ A, double *__restrict__ B, int64_t n,
-                                                   int T, double r, double scale, const unsigned *my_flags,
-                                                   unsigned g, double *put_left, double *put_right,
-                                                   unsigned *flag_left, unsigned *flag_right) {
+                                                   int T, double r, double scale, Guard guard,
+                                                   const unsigned *my_flags, unsigned g, double *put_left,
+                                                   double *put_right, unsigned *flag_left, unsigned *flag_right) {
     __shared__ double w[2][3 * 128];
     const int side = blockIdx.x;  // 0: [0,T) <- left pad; 1: [n-T,n) <- right pad
     if (threadIdx.x == 0) {
@@ -806,14 +645,7 @@ __global__ void __launch_bounds__(96) k3_edges_put(const double *__restrict__ A,
     const int len = 3 * T;
     for (int i = threadIdx.x; i < len; i += blockDim.x) w[0][i] = __ldcv(A + base + i);  // pads: peer-written
     __syncthreads();
-    int cur = 0;
-    for (int s = 0; s < T; ++s) {
-        const int lo = s + 1, hi = len - 1 - s;
-        for (int i = lo + threadIdx.x; i < hi; i += blockDim.x)
-            w[cur ^ 1][i] = eq2<OPS>(w[cur][i - 1], w[cur][i], w[cur][i + 1], r);
-        cur ^= 1;
-        __syncthreads();
-    }
+    const int cur = strip_steps_guarded<OPS>(w, T, r, guard);
     double *put = side == 0 ? put_left : put_right;
     for (int i = threadIdx.x; i < T; i += blockDim.x) {
         double x = w[cur][T + i];
@@ -826,10 +658,10 @@ __global__ void __launch_bounds__(96) k3_edges_put(const double *__restrict__ A,
 }
 
 cudaError_t launch_edges_put(int ops, const double *A, double *B, int64_t n, int T, double q, double scale,
-                             const unsigned *my_flags, unsigned g, double *put_left, double *put_right,
-                             unsigned *flag_left, unsigned *flag_right, cudaStream_t st) {
+                             Guard guard, const unsigned *my_flags, unsigned g, double *put_left,
+                             double *put_right, unsigned *flag_left, unsigned *flag_right, cudaStream_t st) {
     if (T < 1 || T > 128 || n < 2 * (int64_t)T) return cudaErrorInvalidValue;
-#define K3P(o) k3_edges_put<o><<<2, 96, 0, st>>>(A, B, n, T, q, scale, my_flags, g, put_left, put_right, flag_left, flag_right)
+#define K3P(o) k3_edges_put<o><<<2, 96, 0, st>>>(A, B, n, T, q, scale, guard, my_flags, g, put_left, put_right, flag_left, flag_right)
     switch (ops) {
         case 4: K3P(4); break;
         case 3: K3P(3); break;

@@ -1,13 +1,14 @@
 // kernels.h -- internal launcher interface between the runtime (heat1d.cpp)
 // and the sm_100a kernels (kernels.cu).  Not part of the public C ABI.
 #pragma once
+#include <cmath>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace heat1d {
 
 // Arithmetic variants of Eq. 2 (see stencil.cuh).
-enum Ops { OPS_MATCHED4 = 4, OPS_FMA3 = 3, OPS_SCALED2 = 2, OPS_SCALED1 = 1 };
+enum Ops { OPS_LITERAL5 = 5, OPS_MATCHED4 = 4, OPS_FMA3 = 3, OPS_SCALED2 = 2, OPS_SCALED1 = 1 };
 
 // Scaled variants work on v = u / r^t: true iff a pass must end with u = v * r^T'.
 __host__ __device__ constexpr bool ops_scaled(int ops) { return ops <= 2; }
@@ -21,27 +22,48 @@ __host__ __device__ inline double scale_of(double r, int Tp) {
 }
 
 
+// Exactness guard of the contracted matched forms (stencil.cuh): a block of steps runs
+// its OPS only if its cells' keys (GuardAcc) satisfy min(key - 1) >= kmin1 and
+// max(key) <= kmax, else the literal 5-op sequence.  {0, 0xffffffff} = no guard.
+struct Guard {
+    uint32_t kmin1 = 0u, kmax = 0xffffffffu;
+};
+
+// The guard of a block of Tp steps of Eq. 2 with coefficient r in arithmetic `ops`
+// (matched: the result must equal the literal sequence bitwise; fast: no guard).
+inline Guard guard_of(bool matched, int ops, double r, int Tp) {
+    Guard g;
+    if (!matched || (ops != 3 && ops != 4)) return g;
+    // top: max|u| grows by at most G = max(1, 4r) per step (DESIGN.md c3): |x| < 2^(E-1023)
+    const double G = r > 0.5 ? 4.0 * r : 1.0;
+    const double E = 2045.0 - std::ceil((double)Tp * std::log2(G));  // biased exponent bound
+    g.kmax = E < 1.0 ? 0u : (uint32_t)E * (1u << 21) - 1u;
+    // bottom: r = 2^-j, j >= 1, 3-op form: x == 0 or |x| >= 2^(e-1023), e = 1 + j*Tp
+    if (ops == 3 && r > 0.0 && r < 1.0) {
+        int ex = 0;
+        (void)std::frexp(r, &ex);  // r = 0.5 * 2^ex = 2^-j
+        const double e = 1.0 + (double)(1 - ex) * (double)Tp;
+        g.kmin1 = e >= 2047.0 ? 0xffffffffu : (uint32_t)e * (1u << 21) - 1u;
+    }
+    return g;
+}
+
 // Ghost depth (= steps between exchanges) of the inter-warp exchange of pass-kernel
-// kinds 3 (8) and 4 (16); 0 for the other kinds.
+// kinds 3 (8) and 4 (16).
 constexpr int kx_of(int kind) { return kind == 3 ? 8 : kind == 4 ? 16 : 0; }
 
 // Geometry of the temporal-blocked pass kernel (K2) for one launch config.
 struct PassGeom {
     int V;            // cells per thread (odd: conflict-free 64-bit LDS/STS)
-    int NW;           // compute warps per CTA
-    int S;            // TMA pipeline stages (per CTA for kind 0, per warp for kind 1)
+    int NW;           // compute warps per CTA (plus one TMA producer warp)
+    int S;            // TMA pipeline stages per CTA
     int ctas_per_sm;  // resident CTAs per SM the config is sized for (capped by occupancy)
-    int kind = 1;     // 0: CTA tiles (one TMA copy per CTA tile, 2 CTA barriers per tile)
-                      // 1: warp-autonomous spans (each warp its own TMA ring; no CTA barriers)
-                      // 2: CTA tiles + a dedicated TMA producer warp (NW+1 warps per CTA)
-                      // 3, 4: kind 2 + compute warps trade kx_of(kind)-deep ghosts through
-                      //    shared memory every kx_of(kind) steps (only the CTA edges keep the
-                      //    T trapezoid)
+    int kind = 4;     // 3, 4: compute warps trade kx_of(kind)-deep ghosts through shared memory
+                      // every kx_of(kind) steps (only the CTA edges keep the T trapezoid)
     size_t smem_bytes(int T) const;
-    // output cells per scheduling unit (a CTA tile for kind 0, a warp span for kind 1)
+    // output cells per CTA tile
     int64_t tile_out(int T) const {
-        if (kx_of(kind)) return (int64_t)NW * 32 * V - 2 * (int64_t)kx_of(kind) * (NW - 1) - 2 * T;
-        return (kind != 1 ? (int64_t)NW : 1) * (32 * V - 2 * T);
+        return (int64_t)NW * 32 * V - 2 * (int64_t)kx_of(kind) * (NW - 1) - 2 * T;
     }
 };
 
@@ -56,24 +78,26 @@ PassGeom choose_geom(int64_t n_out, int T, int num_sms, int ops);
 // offsets and at [n, n+pad)).  Reads A[out_lo-T, out_hi+T), writes B[out_lo, out_hi).
 // wrapT > 0 (single-slab ring): cells [0,wrapT) are also written to
 // B[n, n+wrapT) and cells [n-wrapT, n) to B[-wrapT, 0)  (periodic self-halo).
-// q = the variant's per-step coefficient, scale = r^T (scaled variants only; stencil.cuh).
+// q = the variant's per-step coefficient, scale = r^T (scaled variants only; stencil.cuh),
+// guard = the exactness guard (guard_of; guarded variants only).
 cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, int64_t n,
                         int T, int64_t out_lo, int64_t out_hi, int wrapT, double q, double scale,
-                        int num_sms, cudaStream_t st, int *grid_out);
+                        Guard guard, int num_sms, cudaStream_t st, int *grid_out);
 
-// K1: one step over the whole ring with modular indexing (no pads used).
+// K1: one step over the whole ring with modular indexing (no pads used); ops 5 (literal,
+// matched mode) or 3 (fast mode).
 cudaError_t launch_naive(int ops, const double *A, double *B, int64_t n, double r, cudaStream_t st);
 
 // K3: the two edge strips [0,T) and [n-T,n) of a slab after its ghosts arrived.
 cudaError_t launch_edges(int ops, const double *A, double *B, int64_t n, int T, double q, double scale,
-                         cudaStream_t st);
+                         Guard guard, cudaStream_t st);
 
 // K3p: K3 fused with a peer-memory halo put (kernels.cu).  my_flags: this slab's two
 // exchange-index words (side 0 at +0, side 1 at +32); put_left/right: where the new
 // left/right strips go in the neighbours' B (their right/left pads); flag_left/right:
 // the neighbours' words for those pads.  Waits for index g, releases g+1.
 cudaError_t launch_edges_put(int ops, const double *A, double *B, int64_t n, int T, double q, double scale,
-                             const unsigned *my_flags, unsigned g, double *put_left, double *put_right,
+                             Guard guard, const unsigned *my_flags, unsigned g, double *put_left, double *put_right,
                              unsigned *flag_left, unsigned *flag_right, cudaStream_t st);
 // Push A[0,T) / A[n-T,n) into the neighbours' pads and release their flags with g+1.
 cudaError_t launch_push_edges(const double *A, int64_t n, int T, unsigned g, double *put_left, double *put_right,
@@ -114,7 +138,7 @@ bool resident_fits(int ops, int64_t n, int T, int num_sms, bool mbox = false);  
 size_t resident_scratch_bytes(int T, int num_sms);
 cudaError_t resident_scratch_init(void *scratch, int T, int num_sms, cudaStream_t st);
 cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
-                            double r, void *scratch, int num_sms, cudaStream_t st, int *warps_out,
+                            double r, Guard guard, void *scratch, int num_sms, cudaStream_t st, int *warps_out,
                             const MboxArgs &mb = MboxArgs{});
 
 }  // namespace heat1d

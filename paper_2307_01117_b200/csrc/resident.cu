@@ -9,13 +9,16 @@
 // and refreshes its halos from its two neighbour spans' edges -- the paper's
 // ghost-zone exchange between segments at depth T, between warps.
 //
-// Synchronisation is pairwise: per-span release/acquire flags in global
-// memory, no grid-wide barrier.  A warp owns SPW = 2 spans half a ring apart
-// and alternates between them (compute A, publish A, refresh B, compute B,
-// publish B, refresh A, ...), so each span's halo exchange is in flight while
-// the warp computes its other span.  Edge buffers are double-buffered by
-// period parity: a span writes period p+2 edges only after its neighbours
-// published p+1, i.e. after they finished reading period p.
+// Synchronisation is pairwise, no grid-wide barrier: spans of V = 17 cells per
+// lane (periods T <= 32) publish their edges with a release of a per-span flag;
+// spans of V >= 33 (the default period T = 64) use data-as-flag slots (below).
+// Edge buffers are double-buffered by period parity: a span writes period p+2
+// edges only after its neighbours published p+1, i.e. after they finished
+// reading period p.
+//
+// Guarded variants (OPS 4, 3; stencil.cuh): at the start of every period a warp
+// checks the cells of its span (owned + halos) and, if any fails, advances that
+// period with the literal 5-op sequence (a warp-uniform branch).
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -62,41 +65,31 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
     return v;
 }
 
-template <int V, int OPS, bool EARLY>
-__device__ __forceinline__ void step_regs(const double (&u)[V], double (&v)[V], double &L, double &R,
-                                          double r) {
-    if constexpr (EARLY) {
-        v[0] = eq2<OPS>(L, u[0], u[1], r);
-        v[V - 1] = eq2<OPS>(u[V - 2], u[V - 1], R, r);
-        L = __shfl_up_sync(0xffffffffu, v[V - 1], 1);
-        R = __shfl_down_sync(0xffffffffu, v[0], 1);
+// One step on the V cells of each lane; the neighbour cells L, R of the lane's
+// outermost cells were fetched by the previous step (shuffles issued early, right
+// after the two outer cells are computed, so their latency hides behind the rest).
+template <int V, int OPS>
+__device__ __forceinline__ void step_regs(const double (&u)[V], double (&v)[V], double &L, double &R, double r) {
+    v[0] = eq2<OPS>(L, u[0], u[1], r);
+    v[V - 1] = eq2<OPS>(u[V - 2], u[V - 1], R, r);
+    L = __shfl_up_sync(0xffffffffu, v[V - 1], 1);
+    R = __shfl_down_sync(0xffffffffu, v[0], 1);
 #pragma unroll
-        for (int j = 1; j < V - 1; ++j) v[j] = eq2<OPS>(u[j - 1], u[j], u[j + 1], r);
-    } else {
-        L = __shfl_up_sync(0xffffffffu, u[V - 1], 1);
-        R = __shfl_down_sync(0xffffffffu, u[0], 1);
-#pragma unroll
-        for (int j = 1; j < V - 1; ++j) v[j] = eq2<OPS>(u[j - 1], u[j], u[j + 1], r);
-        v[0] = eq2<OPS>(L, u[0], u[1], r);
-        v[V - 1] = eq2<OPS>(u[V - 2], u[V - 1], R, r);
-    }
+    for (int j = 1; j < V - 1; ++j) v[j] = eq2<OPS>(u[j - 1], u[j], u[j + 1], r);
 }
 
 // Tp steps on u (v is scratch), result in u; scaled variants end with u *= r^Tp.
-template <int V, int OPS, bool EARLY>
+template <int V, int OPS>
 __device__ __forceinline__ void steps_regs(double (&u)[V], double (&v)[V], int Tp, double r, double scale) {
-    double L = 0.0, R = 0.0;
-    if constexpr (EARLY) {
-        L = __shfl_up_sync(0xffffffffu, u[V - 1], 1);
-        R = __shfl_down_sync(0xffffffffu, u[0], 1);
-    }
+    double L = __shfl_up_sync(0xffffffffu, u[V - 1], 1);
+    double R = __shfl_down_sync(0xffffffffu, u[0], 1);
     int s = 0;
     for (; s + 2 <= Tp; s += 2) {
-        step_regs<V, OPS, EARLY>(u, v, L, R, r);
-        step_regs<V, OPS, EARLY>(v, u, L, R, r);
+        step_regs<V, OPS>(u, v, L, R, r);
+        step_regs<V, OPS>(v, u, L, R, r);
     }
     if (s < Tp) {
-        step_regs<V, OPS, EARLY>(u, v, L, R, r);
+        step_regs<V, OPS>(u, v, L, R, r);
 #pragma unroll
         for (int j = 0; j < V; ++j) u[j] = v[j];
     }
@@ -104,6 +97,42 @@ __device__ __forceinline__ void steps_regs(double (&u)[V], double (&v)[V], int T
 #pragma unroll
         for (int j = 0; j < V; ++j) u[j] = __dmul_rn(u[j], scale);
     }
+}
+
+// The guard's fallback (rare): a period with the literal 5-op sequence on the span's
+// row (which holds the period's input), out of line so that its registers do not add
+// to the hot path's.
+template <int V>
+__device__ __noinline__ void period_literal(double *row, int Tp, double r, int lane) {
+    double u[V], v[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) u[j] = row[lane * V + j];
+    steps_regs<V, 5>(u, v, Tp, r, 1.0);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < V; ++j) row[lane * V + j] = u[j];
+    __syncwarp();
+}
+
+// A period of Tp steps of one span, guarded (stencil.cuh): `live` = the span's row
+// positions holding ring cells (own + 2T; the rest of the 32V registers is slack).
+// The row holds the same cells as u on entry.
+template <int V, int OPS>
+__device__ __forceinline__ void period_steps(double (&u)[V], double (&v)[V], double *row, int Tp, double r,
+                                             double scale, Guard guard, int live, int lane) {
+    if constexpr (ops_guarded(OPS)) {
+        GuardAcc acc;
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+            if (lane * V + j < live) acc.add(u[j]);
+        if (!__all_sync(0xffffffffu, acc.ok(guard))) {
+            period_literal<V>(row, Tp, r, lane);
+#pragma unroll
+            for (int j = 0; j < V; ++j) u[j] = row[lane * V + j];
+            return;
+        }
+    }
+    steps_regs<V, OPS>(u, v, Tp, r, scale);
 }
 
 // One span: its cells [start, start+own) of the ring, staged in `row`
@@ -196,7 +225,7 @@ __device__ __forceinline__ void fence_acq_rel() {
 constexpr unsigned long long HEAT1D_EMPTY_QUIET = HEAT1D_EMPTY | (1ull << 51);
 
 // edges: [Ns][2 parities][2 sides][T]; publish this span's period-p edges
-// (DF: data-as-flag protocol, sync mode 3, compiled into its own kernel instantiation)
+// (DF: data-as-flag protocol, compiled into its own kernel instantiation)
 template <bool DF = false, bool SYS = false>
 __device__ __forceinline__ void publish(const Span &s, int T, unsigned p, double *edges, unsigned *flags,
                                         int lane) {
@@ -303,7 +332,7 @@ __device__ __noinline__ void refresh_df(double *row, int own, int T, double *LE,
 
 template <bool DF = false, bool SYS = false>
 __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, double *edges,
-                                        const unsigned *flags, int lane, int sync, int Ns, const MboxArgs &mb,
+                                        const unsigned *flags, int lane, int Ns, const MboxArgs &mb,
                                         unsigned g, bool initial = false) {
     const bool lrem = mb.on && s.id == 0, rrem = mb.on && s.id == Ns - 1;
     if constexpr (DF) {
@@ -337,21 +366,10 @@ __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, double
     // warp-uniform, so ptxas keeps the step loop's shuffles non-collective.
     // Relaxed polls: an acquire at gpu scope invalidates L1 (CCTL.IVALL) each
     // time; one acquire per flag after the wait orders the edge reads.
-    // sync 0: relaxed polls, then one acquire per flag; 1: acquire polls; 2: relaxed polls,
-    // then one fence (the PTX acquire pattern); tuning knob HEAT1D_K6_SYNC.
-    if (sync == 1) {
-        while (!__all_sync(0xffffffffu, ld_acquire(flags + s.left) >= p + 1 && ld_acquire(flags + s.right) >= p + 1)) {
-        }
-    } else {
-        while (!__all_sync(0xffffffffu, ld_relaxed(flags + s.left) >= p + 1 && ld_relaxed(flags + s.right) >= p + 1)) {
-        }
-        if (sync == 2) {
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        } else {
-            (void)ld_acquire(flags + s.left);
-            (void)ld_acquire(flags + s.right);
-        }
+    while (!__all_sync(0xffffffffu, ld_relaxed(flags + s.left) >= p + 1 && ld_relaxed(flags + s.right) >= p + 1)) {
     }
+    (void)ld_acquire(flags + s.left);
+    (void)ld_acquire(flags + s.right);
     __syncwarp();
     const double *LE = edges + ((size_t)s.left * 4 + (p & 1) * 2) * T + T;  // left's side 1
     const double *RE = edges + ((size_t)s.right * 4 + (p & 1) * 2) * T;     // right's side 0
@@ -365,159 +383,101 @@ __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, double
 }  // namespace
 
 // MB: the cross-rank mailbox code is compiled in (only then: it costs ~30 registers).
-template <int V, int OPS, int SPW, bool EARLY, bool MB = false, bool DF = false>
-__global__ void __launch_bounds__(256, (DF && OPS >= 3) ? 2 : 0)
+// DF: data-as-flag halos (V >= 33 spans).
+template <int V, int OPS, bool MB, bool DF>
+__global__ void __launch_bounds__(256, (DF && OPS >= 3 && V <= 33) ? 2 : 0)
 k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t nt, double r,
-            double rr, double *__restrict__ edges, unsigned *__restrict__ flags, int Wt, int sync, MboxArgs mb_in) {
+            double rr, double *__restrict__ edges, unsigned *__restrict__ flags, int Wt, Guard guard,
+            MboxArgs mb_in) {
     const MboxArgs mb = MB ? mb_in : MboxArgs{};
     extern __shared__ __align__(16) double srow[];
     const int lane = threadIdx.x & 31;
     const int wib = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);  // warp-uniform for the compiler
     const int gw = blockIdx.x * (blockDim.x >> 5) + wib;
     if (gw >= Wt) return;  // whole warps only; no CTA-wide barrier is used below
-    const int Ns = SPW * Wt;
-    double *rows = srow + (size_t)wib * SPW * (32 * V + 1);
+    const int Ns = Wt;
+    double *rows = srow + (size_t)wib * (32 * V + 1);
     const Span a = make_span(gw, Ns, n, rows);
+    const int live = a.own + 2 * T;
     double ua[V], v[V];
     // scaled variants: r is their coefficient c, rr the true r; r^T per full period
     const double scaleT = ops_scaled(OPS) ? scale_of(rr, T) : 1.0;
     load_span<V>(a, A, n, T, lane);
     row_to_regs<V>(a.row, ua, lane);
 
-    if constexpr (SPW == 1) {
-        if (mb.on && (a.id == 0 || a.id == Ns - 1)) {  // outer halos of the initial state: neighbour ranks
-            mbox_publish<DF>(a, Ns, T, mb.base, mb, lane);
-            refresh<DF, MB>(a, T, 0, edges, flags, lane, sync, Ns, mb, mb.base, true);
-            row_to_regs<V>(a.row, ua, lane);
+    if (mb.on && (a.id == 0 || a.id == Ns - 1)) {  // outer halos of the initial state: neighbour ranks
+        mbox_publish<DF>(a, Ns, T, mb.base, mb, lane);
+        refresh<DF, MB>(a, T, 0, edges, flags, lane, Ns, mb, mb.base, true);
+        row_to_regs<V>(a.row, ua, lane);
+    }
+    int64_t done = 0;
+    for (unsigned p = 0;; ++p) {
+        const int Tp = (int)((nt - done) < T ? (nt - done) : T);
+        const double sc = (ops_scaled(OPS) && Tp != T) ? scale_of(rr, Tp) : scaleT;
+        period_steps<V, OPS>(ua, v, a.row, Tp, r, sc, guard, live, lane);
+        regs_to_row<V>(ua, a.row, lane);
+        done += Tp;
+        if (done >= nt) break;
+        // system scope only for the slab's two boundary spans (their halos cross GPUs):
+        // a .sys fence in every warp every period cost more than half of C5's speed
+        if (MB && mb.on && (a.id == 0 || a.id == Ns - 1)) {
+            publish<DF, true>(a, T, p, edges, flags, lane);
+            mbox_publish<DF>(a, Ns, T, mb.base + 1 + p, mb, lane, true);
+            refresh<DF, true>(a, T, p, edges, flags, lane, Ns, mb, mb.base + 1 + p);
+        } else {
+            publish<DF, false>(a, T, p, edges, flags, lane);
+            refresh<DF, false>(a, T, p, edges, flags, lane, Ns, mb, mb.base + 1 + p);
         }
-        int64_t done = 0;
-        for (unsigned p = 0;; ++p) {
-            const int Tp = (int)((nt - done) < T ? (nt - done) : T);
-            const double sc = (ops_scaled(OPS) && Tp != T) ? scale_of(rr, Tp) : scaleT;
-            steps_regs<V, OPS, EARLY>(ua, v, Tp, r, sc);
-            regs_to_row<V>(ua, a.row, lane);
-            done += Tp;
-            if (done >= nt) break;
-            // system scope only for the slab's two boundary spans (their halos cross GPUs):
-            // a .sys fence in every warp every period cost more than half of C5's speed
-            if (MB && mb.on && (a.id == 0 || a.id == Ns - 1)) {
-                publish<DF, true>(a, T, p, edges, flags, lane);
-                mbox_publish<DF>(a, Ns, T, mb.base + 1 + p, mb, lane, true);
-                refresh<DF, true>(a, T, p, edges, flags, lane, sync, Ns, mb, mb.base + 1 + p);
-            } else {
-                publish<DF, false>(a, T, p, edges, flags, lane);
-                refresh<DF, false>(a, T, p, edges, flags, lane, sync, Ns, mb, mb.base + 1 + p);
-            }
-            row_to_regs<V>(a.row, ua, lane);
-        }
+        row_to_regs<V>(a.row, ua, lane);
+    }
 #pragma unroll
-        for (int k = 0; k < V; ++k) {
-            const int q = T + lane + 32 * k;
-            if (q < T + a.own) B[a.start + (q - T)] = a.row[q];
-        }
-    } else {
-        const Span b = make_span(gw + Wt, Ns, n, rows + (32 * V + 1));
-        double ub[V];
-        load_span<V>(b, A, n, T, lane);
-        row_to_regs<V>(b.row, ub, lane);
-        int64_t done = 0;
-        for (unsigned p = 0;; ++p) {
-            const int Tp = (int)((nt - done) < T ? (nt - done) : T);
-            const bool last = done + Tp >= nt;
-            const double sc = (ops_scaled(OPS) && Tp != T) ? scale_of(rr, Tp) : scaleT;
-            steps_regs<V, OPS, EARLY>(ua, v, Tp, r, sc);  // A: halos valid for period p
-            regs_to_row<V>(ua, a.row, lane);
-            if (!last) publish(a, T, p, edges, flags, lane);
-            if (p > 0) {  // B's halos for period p: neighbours' period p-1 edges
-                refresh(b, T, p - 1, edges, flags, lane, sync, Ns, MboxArgs{}, 0u);
-                row_to_regs<V>(b.row, ub, lane);
-            }
-            steps_regs<V, OPS, EARLY>(ub, v, Tp, r, sc);
-            regs_to_row<V>(ub, b.row, lane);
-            if (!last) publish(b, T, p, edges, flags, lane);
-            done += Tp;
-            if (last) break;
-            refresh(a, T, p, edges, flags, lane, sync, Ns, MboxArgs{}, 0u);  // overlapped with B's compute above
-            row_to_regs<V>(a.row, ua, lane);
-        }
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-            const int q = T + lane + 32 * k;
-            if (q < T + a.own) B[a.start + (q - T)] = a.row[q];
-            if (q < T + b.own) B[b.start + (q - T)] = b.row[q];
-        }
+    for (int k = 0; k < V; ++k) {
+        const int q = T + lane + 32 * k;
+        if (q < T + a.own) B[a.start + (q - T)] = a.row[q];
     }
 }
 
 namespace {
 // cells per lane: 17 for periods T <= 32, 33 for 32 < T <= 64, 49 up to 128 (span 32V >= own + 2T)
-int rv_of(int T) {
-    if (const char *e = getenv("HEAT1D_K6_V")) {  // tuning knob: 17, 33 or 49 if the span holds 2T
-        const int v = atoi(e);
-        if ((v == 17 || v == 33 || v == 49) && 32 * v > 2 * T) return v;
-    }
-    return T > 64 ? 49 : T > 32 ? 33 : 17;
-}
-// warps per SM the register budget allows: V=17: ~100 regs (1 span/warp), ~156 (2 spans/warp);
-// V=33: ~128 regs (1 span/warp only)
-int max_wps(int rv, int spw) { return rv == 49 ? 9 : rv == 33 ? 15 : spw == 1 ? 20 : 12; }
+int rv_of(int T) { return T > 64 ? 49 : T > 32 ? 33 : 17; }
+// warps per SM the register budget allows: V=17: ~100 regs; V=33: ~128 regs; V=49: ~220 regs
+int max_wps(int rv) { return rv == 49 ? 9 : rv == 33 ? 15 : 20; }
 constexpr int MAX_WPS_ANY = 20;
 constexpr int MAX_NW = 8;     // warps per CTA (__launch_bounds__(256))
 
 struct ResPlan {
     int64_t wt = 0, nw = 0, grid = 0;
-    int spw = 2, rv = 17;
+    int rv = 17;
     size_t smem = 0;
 };
 
-int res_early() {
-    const char *e = getenv("HEAT1D_K6_EARLY");  // tuning knob
-    return e ? atoi(e) : 1;
+// Data-as-flag halos for V >= 33 spans (every arithmetic form; the matched kernels are
+// compiled with a 2-blocks/SM register target: left alone ptxas gave them ~155 registers
+// and -25 %; profiles/r01_k6_sync3.jsonl).  V = 17 spans (periods T <= 32) keep the flag
+// protocol, whose build keeps three CTAs per SM co-resident for the largest on-chip rings.
+bool res_df(int rv) { return rv >= 33; }
+
+template <int V>
+const void *res_fn_v(int ops, bool mbox) {
+    constexpr bool DF = V >= 33;
+    if (mbox) {
+        switch (ops) {
+            case 4: return (const void *)&k6_resident<V, 4, true, DF>;
+            case 3: return (const void *)&k6_resident<V, 3, true, DF>;
+            case 2: return (const void *)&k6_resident<V, 2, true, DF>;
+            default: return (const void *)&k6_resident<V, 1, true, DF>;
+        }
+    }
+    switch (ops) {
+        case 4: return (const void *)&k6_resident<V, 4, false, DF>;
+        case 3: return (const void *)&k6_resident<V, 3, false, DF>;
+        case 2: return (const void *)&k6_resident<V, 2, false, DF>;
+        default: return (const void *)&k6_resident<V, 1, false, DF>;
+    }
 }
 
-int res_sync() {
-    // halo protocol: 3 (default) = data-as-flag; 0/1/2 = flags with the acquire after the
-    // polls / acquire polls / a fence (tuning knob HEAT1D_K6_SYNC; cross-rank and two-span
-    // kernels always use the flag protocol)
-    const char *e = getenv("HEAT1D_K6_SYNC");
-    return e ? atoi(e) : 3;
-}
-
-// Data-as-flag halos for every arithmetic form (the matched kernels compiled with a
-// 2-blocks/SM register target: left alone ptxas gave them ~155 registers and -25 %;
-// profiles/r01_k6_sync3.jsonl).
-// (V = 17 spans -- periods T <= 32 -- keep the flag protocol: their data-as-flag build lowers
-// the co-resident CTAs per SM and no longer fits the largest on-chip rings.)
-bool res_df(int rv) { return res_sync() == 3 && res_early() != 0 && rv >= 33; }
-
-const void *res_fn(int ops, int spw, int rv, bool mbox = false, bool df = false) {
-    if (df && !mbox && spw == 1) {  // data-as-flag halos (early shuffles)
-#define RFD(v) (ops == 4 ? (const void *)&k6_resident<v, 4, 1, true, false, true> : ops == 3 ? (const void *)&k6_resident<v, 3, 1, true, false, true> \
-                : ops == 2 ? (const void *)&k6_resident<v, 2, 1, true, false, true> : (const void *)&k6_resident<v, 1, 1, true, false, true>)
-        return rv == 49 ? RFD(49) : rv == 33 ? RFD(33) : RFD(17);
-#undef RFD
-    }
-    if (mbox && df) {  // SPW = 1, early shuffles, mailbox + data-as-flag across GPUs
-#define RFMD(v) (ops == 4 ? (const void *)&k6_resident<v, 4, 1, true, true, true> : ops == 3 ? (const void *)&k6_resident<v, 3, 1, true, true, true> \
-                 : ops == 2 ? (const void *)&k6_resident<v, 2, 1, true, true, true> : (const void *)&k6_resident<v, 1, 1, true, true, true>)
-        return rv == 49 ? RFMD(49) : RFMD(33);
-#undef RFMD
-    }
-    if (mbox) {  // SPW = 1, early shuffles, mailbox code compiled in
-#define RFM(v) (ops == 4 ? (const void *)&k6_resident<v, 4, 1, true, true> : ops == 3 ? (const void *)&k6_resident<v, 3, 1, true, true> \
-                : ops == 2 ? (const void *)&k6_resident<v, 2, 1, true, true> : (const void *)&k6_resident<v, 1, 1, true, true>)
-        return rv == 49 ? RFM(49) : rv == 33 ? RFM(33) : RFM(17);
-#undef RFM
-    }
-    const bool early = res_early() != 0;
-#define RF(v, o, s, e) (const void *)&k6_resident<v, o, s, e>
-#define RF_OPS(v, s, e) (ops == 4 ? RF(v, 4, s, e) : ops == 3 ? RF(v, 3, s, e) : ops == 2 ? RF(v, 2, s, e) : RF(v, 1, s, e))
-    if (rv == 49) return early ? RF_OPS(49, 1, true) : RF_OPS(49, 1, false);
-    if (rv == 33) return early ? RF_OPS(33, 1, true) : RF_OPS(33, 1, false);
-    if (spw == 1) return early ? RF_OPS(17, 1, true) : RF_OPS(17, 1, false);
-    return early ? RF_OPS(17, 2, true) : RF_OPS(17, 2, false);
-#undef RF_OPS
-#undef RF
+const void *res_fn(int ops, int rv, bool mbox) {
+    return rv == 49 ? res_fn_v<49>(ops, mbox) : rv == 33 ? res_fn_v<33>(ops, mbox) : res_fn_v<17>(ops, mbox);
 }
 
 cudaError_t res_attr(const void *fn) {  // raise the dynamic shared-memory limit once per kernel
@@ -527,53 +487,47 @@ cudaError_t res_attr(const void *fn) {  // raise the dynamic shared-memory limit
     for (const void *d : done)
         if (d == fn) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         2 * 16 * (32 * 17 + 1) * 8);  // >= 8 warps x (32*49+1) too
+                                         MAX_NW * (32 * 49 + 1) * 8);
     if (e == cudaSuccess) done.push_back(fn);
     return e;
 }
 
-// Split the ring into Ns = spw*Wt equal spans (each owning >= T cells, span
-// own + 2T <= 32*RV) with warps balanced across SMs.
+// Split the ring into Ns = Wt equal spans (each owning >= T cells, span own + 2T <= 32*RV)
+// with warps balanced across SMs, one span per warp.
 bool res_plan(int ops, int64_t n, int T, int num_sms, ResPlan *p, bool mbox = false) {
     const int RV = rv_of(T);
     p->rv = RV;
     const int cap = 32 * RV - 2 * T;
     if (T < 1 || cap <= 0 || n < T) return false;
-    // 1 span per warp by default (profiles/r01_k6_ab_*.jsonl: 2 spans per warp do
-    // not pay on B200); HEAT1D_K6_SPW=2 selects the alternating two-span warps.
-    p->spw = 1;
-    if (const char *e = getenv("HEAT1D_K6_SPW"))
-        p->spw = (atoi(e) == 2 && n >= 2 * (int64_t)T && RV == 17 && !mbox) ? 2 : 1;
-    const int64_t ns_min = (n + cap - 1) / cap;
-    const int64_t wt_min = (ns_min + p->spw - 1) / p->spw;
+    const int64_t wt_min = (n + cap - 1) / cap;
     if (wt_min <= num_sms) {
         p->wt = wt_min;  // one warp per CTA, each on its own SM
         p->nw = 1;
         p->grid = p->wt;
     } else {
         const int64_t wps = (wt_min + num_sms - 1) / num_sms;
-        if (wps > max_wps(RV, p->spw)) return false;
+        if (wps > max_wps(RV)) return false;
         const int64_t cps = (wps + MAX_NW - 1) / MAX_NW;  // CTAs per SM (blocks <= 8 warps)
         p->nw = (wps + cps - 1) / cps;
         p->grid = (int64_t)num_sms * cps;
         p->wt = p->grid * p->nw;
     }
-    while (p->wt > 1 && n / (p->wt * p->spw) < T) {
+    while (p->wt > 1 && n / p->wt < T) {
         p->wt = (p->wt + 1) / 2;
         p->nw = 1;
         p->grid = p->wt;
     }
-    const int64_t ns = p->wt * p->spw;
+    const int64_t ns = p->wt;
     if (n / ns < T || n / ns + (n % ns ? 1 : 0) + 2 * T > 32 * RV) return false;
-    p->smem = (size_t)p->nw * p->spw * (32 * RV + 1) * sizeof(double);
-    const void *fn = res_fn(ops, p->spw, RV, mbox, res_df(RV));
+    p->smem = (size_t)p->nw * (32 * RV + 1) * sizeof(double);
+    const void *fn = res_fn(ops, RV, mbox);
     if (res_attr(fn) != cudaSuccess) return false;
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, (int)(p->nw * 32), p->smem) != cudaSuccess)
         return false;
     if (getenv("HEAT1D_DEBUG"))
-        fprintf(stderr, "[heat1d] K6 plan n=%lld T=%d V=%d ops=%d spw=%d wt=%lld nw=%lld grid=%lld occ=%d smem=%zu\n",
-                (long long)n, T, RV, ops, p->spw, (long long)p->wt, (long long)p->nw, (long long)p->grid, occ, p->smem);
+        fprintf(stderr, "[heat1d] K6 plan n=%lld T=%d V=%d ops=%d wt=%lld nw=%lld grid=%lld occ=%d smem=%zu\n",
+                (long long)n, T, RV, ops, (long long)p->wt, (long long)p->nw, (long long)p->grid, occ, p->smem);
     return (int64_t)occ * num_sms >= p->grid;  // cooperative launch: all CTAs co-resident
 }
 
@@ -581,8 +535,7 @@ bool res_plan(int ops, int64_t n, int T, int num_sms, ResPlan *p, bool mbox = fa
 
 int64_t resident_capacity(int T, int num_sms) {
     const int rv = rv_of(T);
-    const int64_t a = max_wps(rv, 1), b = rv == 17 ? 2 * (int64_t)max_wps(rv, 2) : 0;
-    return (int64_t)num_sms * (a > b ? a : b) * (32 * rv - 2 * T);
+    return (int64_t)num_sms * max_wps(rv) * (32 * rv - 2 * T);
 }
 
 bool resident_fits(int ops, int64_t n, int T, int num_sms, bool mbox) {
@@ -596,14 +549,14 @@ __global__ void k6_fill_empty(double *edges, int64_t count) {
 }
 
 size_t resident_scratch_bytes(int T, int num_sms) {
-    const int64_t ns = (int64_t)num_sms * 2 * MAX_WPS_ANY;
+    const int64_t ns = (int64_t)num_sms * (MAX_WPS_ANY + MAX_NW);  // >= any plan's wt
     return (size_t)ns * 4 * T * sizeof(double) + (size_t)ns * sizeof(unsigned) + 256;
 }
 
 cudaError_t resident_scratch_init(void *scratch, int T, int num_sms, cudaStream_t st) {
     // every edge slot of the largest plan EMPTY once per handle: a complete run consumes and
     // resets every slot it publishes, so the data-as-flag invariant holds from run to run
-    const int64_t ns = (int64_t)num_sms * 2 * MAX_WPS_ANY;
+    const int64_t ns = (int64_t)num_sms * (MAX_WPS_ANY + MAX_NW);  // >= any plan's wt
     k6_fill_empty<<<148, 256, 0, st>>>(static_cast<double *>(scratch), ns * 4 * (int64_t)T);
     return cudaGetLastError();
 }
@@ -617,29 +570,23 @@ cudaError_t launch_mbox_init(double *mbox, cudaStream_t st) {  // every data slo
 }
 
 cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
-                            double r, void *scratch, int num_sms, cudaStream_t st, int *warps_out,
+                            double r, Guard guard, void *scratch, int num_sms, cudaStream_t st, int *warps_out,
                             const MboxArgs &mb) {
     ResPlan p;
     if (!res_plan(ops, n, T, num_sms, &p, mb.on != 0)) return cudaErrorInvalidValue;
-    const int64_t ns = p.wt * p.spw;
+    const int64_t ns = p.wt;
     double *edges = static_cast<double *>(scratch);
     unsigned *flags = reinterpret_cast<unsigned *>(edges + (size_t)ns * 4 * T);
     cudaError_t e = cudaMemsetAsync(flags, 0, (size_t)ns * sizeof(unsigned), st);
     if (e != cudaSuccess) return e;
     int Wt = (int)p.wt;
-    int sync = res_sync();
-    const bool df = res_df(p.rv) && p.spw == 1;  // data-as-flag kernel (local and mailbox halos)
-    if (sync == 3 && !df) sync = 0;
     // (data-as-flag: the edge slots are EMPTY already -- resident_scratch_init at create, and
     // every completed launch leaves them so)
     void *args[] = {(void *)&A, (void *)&B, (void *)&n, (void *)&T, (void *)&nt, (void *)&q, (void *)&r,
-                    (void *)&edges, (void *)&flags, (void *)&Wt, (void *)&sync, (void *)&mb};
+                    (void *)&edges, (void *)&flags, (void *)&Wt, (void *)&guard, (void *)&mb};
     if (warps_out) *warps_out = Wt;
-    if (getenv("HEAT1D_DEBUG"))
-        fprintf(stderr, "[heat1d] K6 n=%lld T=%d spw=%d Wt=%d nw=%lld grid=%lld smem=%zu\n", (long long)n, T,
-                p.spw, Wt, (long long)p.nw, (long long)p.grid, p.smem);
-    return cudaLaunchCooperativeKernel(res_fn(ops, p.spw, p.rv, mb.on != 0, df), dim3((unsigned)p.grid), dim3((unsigned)(p.nw * 32)),
-                                       args, p.smem, st);
+    return cudaLaunchCooperativeKernel(res_fn(ops, p.rv, mb.on != 0), dim3((unsigned)p.grid),
+                                       dim3((unsigned)(p.nw * 32)), args, p.smem, st);
 }
 
 }  // namespace heat1d

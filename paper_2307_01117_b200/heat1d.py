@@ -21,7 +21,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libheat1d.so")
+LIB_PATH = os.environ.get("HEAT1D_LIB") or os.path.join(_HERE, "libheat1d.so")  # override: A/B builds (tools/)
 
 OK, EINVAL, EUNSTABLE, ESTATE, ENOMEM, ECUDA, ENCCL, EUNSUPPORTED = range(8)
 MODES = {"matched": 0, "fast": 1}

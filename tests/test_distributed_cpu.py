@@ -133,11 +133,14 @@ def _worker_light_cone(rank, world, port, N, nt, k, seed, out_q):
         import synth
         first, count = h1.partition(N, 1, world, rank)
         u = torch.from_numpy(synth.uniform(seed, first, count, -1.0, 1.0))
-        left, right = (rank - 1) % world, (rank + 1) % world
-        s_last, s_first = u[count - nt:].clone(), u[:nt].clone()
+        # the library's own plan at depth nt (heat1d_plan_exchange; heat1d_solve_host issues it)
+        pl = h1.plan_exchange(N, 1, world, rank, nt)
+        assert pl.cells == nt and pl.recv_left_off == -nt and pl.recv_right_off == count
+        s_last = u[pl.send_right_off:pl.send_right_off + nt].clone()
+        s_first = u[pl.send_left_off:pl.send_left_off + nt].clone()
         r_left, r_right = torch.empty(nt, dtype=torch.float64), torch.empty(nt, dtype=torch.float64)
-        reqs = [dist.isend(s_last, right), dist.isend(s_first, left), dist.irecv(r_left, left),
-                dist.irecv(r_right, right)]
+        reqs = [dist.isend(s_last, pl.right), dist.isend(s_first, pl.left), dist.irecv(r_left, pl.left),
+                dist.irecv(r_right, pl.right)]
         for q in reqs:
             q.wait()
         w0 = np.concatenate([r_left.numpy(), u.numpy(), r_right.numpy()])
