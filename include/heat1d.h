@@ -152,95 +152,145 @@ typedef struct {
     int64_t cells;              /* T cells per message (8T bytes)                           */
 } heat1d_exchange_plan;
 
+/* Citation key: P:NN = PAPER.md line NN (Section 2 "Model problem": Eq. 1 at P:61, Eq. 2 at
+ * P:66-70, the grid at P:64-65, u(0,x_i) = x_i and the periodic loop at P:71, the segmented
+ * ghost-zone algorithm at; "cells processed per second" at P:228).  Unless stated,
+ * every call returns HEAT1D_EINVAL for a NULL handle / output pointer and leaves all state
+ * unchanged on EINVAL; ECUDA / ENCCL poison the handle. */
+
+/* Fill *o with the defaults (matched mode, D = dx^2, auto T, one rank, P2P transport).
+ * NULL-safe.  Not from the paper: the ABI's option conventions. */
 HEAT1D_API void heat1d_opts_default(heat1d_opts *o);
 HEAT1D_API int heat1d_version(void);
+/* Static string for a status code (never NULL). */
 HEAT1D_API const char *heat1d_strerror(int status);
 
-/* Slab of `rank` when N = nx*np cells are split over `nranks` contiguous slabs:
+/* Slab [*first, *first + *count) of `rank` when the ring of N = nx*np cells (the paper's
+ * np segments of nx cells) is split over `nranks` contiguous slabs:
  * partition-granular and front-loaded when np >= nranks, else
- * cell-granular front-loaded.  Pure host function. */
+ * cell-granular front-loaded.  Pure host function (no GPU).  EINVAL: nx < 1, np < 1,
+ * N > 2^62, rank outside [0, nranks), or fewer cells than slabs. */
 HEAT1D_API int heat1d_partition(int64_t nx, int64_t np, int32_t nranks, int32_t rank,
                      int64_t *first, int64_t *count);
 
-/* Message plan of `rank` for one exchange of depth T (pure host function).
- * Order matters when left == right (nranks == 2): NCCL and the reference CPU
- * model issue send(right edge), send(left edge), recv(left pad), recv(right pad). */
+/* The ghost-zone exchange of P:73 at depth T: the four messages of `rank` (offsets in cells
+ * from cell 0 of its slab; negative = left pad).  Pure host function, and the single
+ * source of the offsets every exchange the library issues uses.  Order matters when
+ * left == right (nranks == 2): send(right edge), send(left edge), recv(left pad),
+ * recv(right pad).  EINVAL: as heat1d_partition, T < 1, or T > the smallest slab. */
 HEAT1D_API int heat1d_plan_exchange(int64_t nx, int64_t np, int32_t nranks, int32_t rank, int32_t T,
                          heat1d_exchange_plan *plan);
 
 /* Doubles of device memory a handle with these arguments needs for its state (both
- * ping-pong buffers of every local slab, pads for T = opts->T or, if 0, HEAT1D_T_MAX):
- * the minimum size of opts->dev_buf.  -1 on invalid arguments. */
+ * ping-pong buffers of every local slab -- the Jacobi double buffer of Eq. 2, which reads
+ * time-t values only, P:68 -- with pads for T = opts->T or, if 0, HEAT1D_T_MAX): the
+ * minimum size of opts->dev_buf.  opts may be NULL (defaults).  -1 on invalid arguments. */
 HEAT1D_API int64_t heat1d_buffer_len(int64_t nx, int64_t np, const heat1d_opts *opts);
 
-/* rank 0 only: writes a 128-byte ncclUniqueId to out128 (host memory). */
+/* rank 0 only: writes a 128-byte ncclUniqueId to out128 (caller-owned host memory), to be
+ * broadcast to every rank's opts.nccl_id.  ENCCL if NCCL fails.  (Plumbing, not the paper.) */
 HEAT1D_API int heat1d_get_unique_id(void *out128);
 
-/* Validate, compute r, allocate 2 buffers of (count + 2*pad) fp64 per slab,
- * create streams/events, and (nranks > 1) join the NCCL ring -- collective
- * over all ranks.  nt is the default step count of heat1d_run(h, -1).
- * Errors: EINVAL (nx<1, np<1, N>2^62, nt<0, k<0, dt<=0, dx<=0, non-finite,
- * bad rank/nranks/T/virtual_slabs, count < T... see DESIGN.md §5), EUNSTABLE
- * (r > 1/2), ENOMEM, ECUDA, ENCCL.  On error *out = NULL. */
+/* Set up the model problem of P:57-71 for nt steps: N = nx*np grid points x_i = i*dx
+ * (P:64-65), diffusivity k (alpha) and time step dt, r = (k*dt)/(dx*dx) computed once
+ * on the host in fp64 (Eq. 2, with the denominator of DESIGN.md reading c1; the
+ * literal "2h" is opts->denominator = HEAT1D_DEN_PAPER_2DX).  Validates, picks T and the
+ * kernel family (agreed over the ranks), allocates 2 buffers of (count + 2*pad) fp64 per
+ * slab (or uses opts->dev_buf), creates streams/events and, with nranks > 1, joins the
+ * NCCL ring and maps the neighbours' memory -- collective over all ranks.  nt is the
+ * default step count of heat1d_run(h, -1).  On error *out = NULL.
+ * Errors: EINVAL (nx < 1, np < 1, N > 2^62, nt < 0, k < 0, dt <= 0, dx <= 0, non-finite
+ * arguments, bad rank/nranks/T/virtual_slabs/mode, nranks > 1 without nccl_id), EUNSTABLE
+ * (r > 1/2 without allow_unstable), EUNSUPPORTED (a combination this build does
+ * not run, e.g. resident = 1 for a slab that does not fit), ENOMEM, ECUDA, ENCCL. */
 HEAT1D_API int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt,
                   double k, double dt, double dx, const heat1d_opts *opts);
 
-/* This handle's slab [first, first+count) of the ring. */
+/* This handle's slab [*first, *first + *count) of the ring (heat1d_partition of its rank;
+ * all virtual slabs together).  Host-only, never fails on a valid handle. */
 HEAT1D_API int heat1d_local_range(heat1d_t h, int64_t *first, int64_t *count);
 
-/* Copy u(0) of this rank's slab (count = local count, host or device pointer).
- * The data is COPIED before return; the caller may free u0 at once.
- * Resets steps_done to 0. */
+/* The initial condition u(0, x_i) of this rank's slab (P:71 gives u(0, x_i) = x_i; any
+ * values are accepted).  u0: `count` (= the local slab) fp64 values, host or device
+ * pointer, COPIED before return (the caller may free u0 at once; the caller owns it).
+ * Resets steps_done to 0; in fast mode checks max|u0| (K5, DESIGN.md c21).
+ * EINVAL: NULL u0 or count != local count.  EUNSUPPORTED on a streaming handle. */
 HEAT1D_API int heat1d_set_initial(heat1d_t h, const double *u0, int64_t count);
 
-/* Device-side initial condition u0[i] = lo + (hi-lo)*U(seed, i) for the global
- * cell indices i of this slab, U = splitmix64 counter form (DESIGN.md §4,
- * identical to synth.uniform).  Resets steps_done to 0. */
+/* Device-side initial condition u0[i] = lo + (hi-lo)*U(seed, i) for the global cell
+ * indices i of this slab, U = splitmix64 counter form (reading c12 for
+ * BASELINE.json's "uniform from seed s"; identical to synth.uniform).  Not from the
+ * paper: the synthetic inputs of BASELINE.json configs[1], [3].  Resets steps_done.
+ * EINVAL on non-finite lo/hi. */
 HEAT1D_API int heat1d_init_uniform(heat1d_t h, uint64_t seed, double lo, double hi);
 
-/* Advance nt >= 0 steps (cumulative over calls; nt < 0 = create's nt).
- * Collective over ranks when nranks > 1.  ESTATE before an initial state. */
+/* Advance nt >= 0 steps of Eq. 2 on the periodic loop, cumulative over
+ * calls (nt < 0 = create's nt): T steps per pass over the state, depth-T ghost zones
+ * exchanged between slabs every T steps -- the segmented algorithm of P:73 at depth T.
+ * Matched mode is bitwise equal to nt sweeps of the literal update (the oracle) for any
+ * T, slab and rank count.  Blocking by default (opts.blocking).  Collective over ranks
+ * when nranks > 1.  ESTATE before an initial state; ECUDA/ENCCL poison the handle. */
 HEAT1D_API int heat1d_run(heat1d_t h, int64_t nt);
 
-/* Copy this slab's current state to out (host or device pointer), synchronous. */
+/* Copy this slab's current state u(t, x_i) (t = steps_done) to out: `count` (= the local
+ * slab) fp64, host or device pointer, caller-owned; synchronous.  EINVAL: NULL out or
+ * count mismatch.  ESTATE before an initial state. */
 HEAT1D_API int heat1d_get(heat1d_t h, double *out, int64_t count);
 
 /* One whole solve between HOST arrays with the transfers hidden behind the compute:
  * u0 (count = local n cells) -> nt steps -> out (count cells); same result as
  * heat1d_set_initial(u0) + heat1d_run(nt) + heat1d_get(out) (bitwise in matched mode).
- * By the domain of dependence of Eq. 2 (a cell at step t depends on
- * cells within t of it at step 0), the ring is cut into C chunks and each chunk is
- * solved on its own light-cone window [chunk - nt, chunk + nt) (indices mod N); the
- * H2D copy of window c+1 and the D2H copy of chunk c-1 run on their own streams while
- * window c computes, so a solve costs ~max(transfers, compute) instead of their sum.
- * Used for one slab per rank when the chunks are >= 16 nt cells (redundant work
- * <= 2nt/chunk); with nranks > 1 the ranks first trade nt-deep halos once (NCCL) and then
- * stream independently (collective; every rank takes the same branch); otherwise it IS
- * the plain three-call sequence.  u0/out should be
- * pinned (cudaHostAlloc / torch pin_memory) for the copies to overlap.  In fast mode
- * every window checks its own max|u0| (K5) and is recomputed with the 3-op form if
- * the scaled state could overflow (DESIGN.md c21).  Afterwards the device state is
- * consumed: call set_initial before run/get.  u0 and out must not overlap (EINVAL).
- * Errors as set_initial/run/get. */
+ * By the domain of dependence of Eq. 2 (a cell at step t depends on cells within t
+ * of it at step 0), the ring is cut into C chunks and each chunk is solved on its own
+ * light-cone window [chunk - nt, chunk + nt) (indices mod N); the H2D copy of window c+1
+ * and the D2H copy of chunk c-1 run on their own streams while window c computes, so a
+ * solve costs ~max(transfers, compute) instead of their sum.  Used for one slab per rank
+ * when the chunks are >= 16 nt cells and nt <= the slab (redundant work <= 2nt/chunk);
+ * with nranks > 1 the ranks first trade nt-deep halos once (the plan of
+ * heat1d_plan_exchange at depth nt, NCCL; collective, every rank takes the same branch);
+ * otherwise it IS the plain three-call sequence.  u0/out (caller-owned) should be pinned
+ * (cudaHostAlloc / torch pin_memory) for the copies to overlap.  In fast mode every
+ * window checks its own max|u0| (K5) and is recomputed with the 3-op form if the scaled
+ * state could overflow (DESIGN.md c21).  Afterwards the device state is consumed: call
+ * set_initial before run/get.  EINVAL: NULL or overlapping u0/out, count mismatch.
+ * EUNSUPPORTED: a streaming handle whose window cannot hold nt.  Else as run. */
 HEAT1D_API int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, double *out);
 
 /* heat1d_solve_host for ONE slab whose neighbour cells the caller supplies: left = the nt
  * cells preceding the slab (left[nt-1] next to u0[0]), right = the nt cells following it
- * (host or device pointers).  The result depends on nothing else (the light cone of nt
- * steps), so a caller that decomposes a ring itself needs no further communication.
- * With nranks > 1 heat1d_solve_host does exactly this after one NCCL exchange of the
- * nt-deep halos (collective).  EUNSUPPORTED if the slab is too small for the windows. */
+ * (host or device pointers, caller-owned).  The result depends on nothing else (the light
+ * cone of nt steps), so a caller that decomposes a ring itself needs no further
+ * communication.  EUNSUPPORTED if the slab is too small for the windows. */
 HEAT1D_API int heat1d_solve_host_halo(heat1d_t h, const double *u0, const double *left, const double *right,
                                       int64_t count, int64_t nt, double *out);
 
-HEAT1D_API int64_t heat1d_steps_done(heat1d_t h);   /* -1 if h is NULL */
+/* Steps advanced since the last initial state (t of u(t, x_i)); -1 if h is NULL. */
+HEAT1D_API int64_t heat1d_steps_done(heat1d_t h);
+/* Read-only facts (heat1d_info_t); info->size must equal sizeof(heat1d_info_t) (EINVAL). */
 HEAT1D_API int heat1d_info(heat1d_t h, heat1d_info_t *info);
 
-/* Per-launch timing of the dominant (pass) kernel with CUDA events on the
- * compute stream.  heat1d_profile returns launches and summed milliseconds
- * since profiling was enabled (synchronises the stream). */
+/* Profiling: while on, every kernel group is bracketed by CUDA events on
+ * the stream it runs on -- the interior pass K2 / the resident K6 / K1 on the compute
+ * stream, the halo exchange + edge strips (K3/K3p, several slabs) on the comm stream.
+ * CUDA graphs are bypassed while profiling.  heat1d_set_profiling(h, 1) resets the totals
+ * and the trace and records the trace's time origin on the compute stream.
+ * heat1d_profile: launches and summed milliseconds of the compute-stream groups (the
+ * dominant kernel) since profiling was enabled (synchronises both streams). */
 HEAT1D_API int heat1d_set_profiling(heat1d_t h, int on);
 HEAT1D_API int heat1d_profile(heat1d_t h, int64_t *launches, double *ms);
+
+enum { HEAT1D_TRACE_K1 = 1, HEAT1D_TRACE_K2 = 2, HEAT1D_TRACE_HALO = 3, HEAT1D_TRACE_K6 = 6 };
+typedef struct {
+    int32_t stream;         /* 0 = compute stream, 1 = comm stream                          */
+    int32_t kind;           /* HEAT1D_TRACE_*                                               */
+    double t0_ms, t1_ms;    /* interval, ms after heat1d_set_profiling(h, 1)                */
+} heat1d_trace_event;
+
+/* The profiling session's intervals (the overlap timeline of the two streams; the
+ * first min(cap, *count) are copied to events, caller-owned host memory; at most 2^20
+ * are kept).  *count = how many exist.  EINVAL on NULL count (or NULL events with
+ * cap > 0); synchronises both streams. */
+HEAT1D_API int heat1d_trace(heat1d_t h, heat1d_trace_event *events, int64_t cap, int64_t *count);
 
 /* Compute stream of the handle as a cudaStream_t (for the caller's events). */
 HEAT1D_API void *heat1d_stream(heat1d_t h);

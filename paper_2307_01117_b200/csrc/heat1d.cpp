@@ -112,8 +112,17 @@ struct heat1d_s {
     std::vector<Graph> graphs;
 
     bool prof = false;
-    std::vector<cudaEvent_t> ev_pool;
-    size_t ev_used = 0;
+    // profiling (heat1d_set_profiling): CUDA-event pairs around every kernel group, on the
+    // stream it runs on; collected into the dominant kernel's totals and a trace
+    struct ProfRec {
+        cudaEvent_t a, b;
+        int stream, kind;
+    };
+    std::vector<cudaEvent_t> ev_pool;  // free events
+    std::vector<cudaEvent_t> ev_all;   // every event created (destroyed with the handle)
+    std::vector<ProfRec> prof_recs;    // recorded, not yet collected
+    cudaEvent_t prof_t0 = nullptr;     // the trace's time origin (compute stream)
+    std::vector<heat1d_trace_event> trace;
     int64_t prof_launches = 0;
     double prof_ms = 0.0;
 
@@ -261,24 +270,58 @@ bool parse_geom_env(PassGeom *g) {
 }
 
 cudaEvent_t prof_event(heat1d_t h) {
-    if (h->ev_used == h->ev_pool.size()) {
+    if (h->ev_pool.empty()) {
         cudaEvent_t e;
         if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
-        h->ev_pool.push_back(e);
+        h->ev_all.push_back(e);
+        return e;
     }
-    return h->ev_pool[h->ev_used++];
+    cudaEvent_t e = h->ev_pool.back();
+    h->ev_pool.pop_back();
+    return e;
 }
 
+// Open a profiled interval on stream `st` (no-op unless profiling); close it with prof_end.
+int prof_begin(heat1d_t h, cudaStream_t st, heat1d_s::ProfRec *rec, int stream_id, int kind) {
+    rec->a = rec->b = nullptr;
+    if (!h->prof) return HEAT1D_OK;
+    rec->a = prof_event(h);
+    rec->b = prof_event(h);
+    rec->stream = stream_id;
+    rec->kind = kind;
+    if (!rec->a || !rec->b) return set_error(h, HEAT1D_ECUDA, "event pool");
+    CK(cudaEventRecord(rec->a, st));
+    return HEAT1D_OK;
+}
+
+int prof_end(heat1d_t h, cudaStream_t st, const heat1d_s::ProfRec &rec) {
+    if (!h->prof || !rec.b) return HEAT1D_OK;
+    CK(cudaEventRecord(rec.b, st));
+    h->prof_recs.push_back(rec);
+    return HEAT1D_OK;
+}
+
+constexpr size_t kTraceMax = 1 << 20;  // trace entries kept per profiling session
+
 int prof_collect(heat1d_t h) {
-    if (h->ev_used == 0) return HEAT1D_OK;
+    if (h->prof_recs.empty()) return HEAT1D_OK;
     CK(cudaStreamSynchronize(h->stream));
-    for (size_t i = 0; i + 1 < h->ev_used; i += 2) {
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, h->ev_pool[i], h->ev_pool[i + 1]));
-        h->prof_ms += ms;
-        h->prof_launches += 1;
+    if (h->comm) CK(cudaStreamSynchronize(h->comm));
+    for (const auto &r : h->prof_recs) {
+        float ms = 0.f, t0 = 0.f;
+        CK(cudaEventElapsedTime(&ms, r.a, r.b));
+        if (r.stream == 0) {  // the dominant kernel: the interior pass K2 or the resident K6
+            h->prof_ms += ms;
+            h->prof_launches += 1;
+        }
+        if (h->prof_t0 && h->trace.size() < kTraceMax) {
+            CK(cudaEventElapsedTime(&t0, h->prof_t0, r.a));
+            h->trace.push_back(heat1d_trace_event{r.stream, r.kind, (double)t0, (double)t0 + ms});
+        }
+        h->ev_pool.push_back(r.a);
+        h->ev_pool.push_back(r.b);
     }
-    h->ev_used = 0;
+    h->prof_recs.clear();
     return HEAT1D_OK;
 }
 
@@ -289,21 +332,16 @@ heat1d::Guard guard_for(heat1d_t h, int ops, int Tp) {
 }
 
 int launch_pass_slab(heat1d_t h, const Slab &s, int Tp, int64_t lo, int64_t hi, int wrapT) {
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (h->prof) {
-        e0 = prof_event(h);
-        e1 = prof_event(h);
-        if (!e0 || !e1) return set_error(h, HEAT1D_ECUDA, "event pool");
-        CK(cudaEventRecord(e0, h->stream));
-    }
+    heat1d_s::ProfRec rec;
+    int rc = prof_begin(h, h->stream, &rec, 0, HEAT1D_TRACE_K2);
+    if (rc) return rc;
     int grid = 0;
     CK(heat1d::launch_pass(h->geom, h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp, lo, hi,
                            wrapT, h->q, heat1d::scale_of(h->r, Tp), guard_for(h, h->ops, Tp), h->num_sms,
                            h->stream, &grid));
     if (grid > 0) h->launches++;
     h->last_grid = grid > 0 ? grid : h->last_grid;
-    if (h->prof) CK(cudaEventRecord(e1, h->stream));
-    return HEAT1D_OK;
+    return prof_end(h, h->stream, rec);
 }
 
 // Fill the depth-Tp ghost pads of every slab of the current buffer from the
@@ -340,13 +378,9 @@ int exchange(heat1d_t h, int Tp) {
 
 int run_resident(heat1d_t h, int64_t nt) {
     const Slab &s = h->slabs[0];
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (h->prof) {
-        e0 = prof_event(h);
-        e1 = prof_event(h);
-        if (!e0 || !e1) return set_error(h, HEAT1D_ECUDA, "event pool");
-        CK(cudaEventRecord(e0, h->stream));
-    }
+    heat1d_s::ProfRec rec;
+    int rc = prof_begin(h, h->stream, &rec, 0, HEAT1D_TRACE_K6);
+    if (rc) return rc;
     heat1d::MboxArgs mb;
     if (h->mbox) {
         mb.self = h->mbox;
@@ -363,7 +397,8 @@ int run_resident(heat1d_t h, int64_t nt) {
                                h->r, guard_for(h, h->ops, h->T), h->res_scratch, h->num_sms, h->stream,
                                &h->res_warps, mb));
     h->launches++;
-    if (h->prof) CK(cudaEventRecord(e1, h->stream));
+    rc = prof_end(h, h->stream, rec);
+    if (rc) return rc;
     h->cur ^= 1;
     // (no periodic pads to refresh: K6 reads its halos modularly and a resident handle never
     // runs another kernel family)
@@ -378,17 +413,15 @@ int run_passes(heat1d_t h, int64_t nt) {
     while (done < nt) {
         if (h->kernel == HEAT1D_KERNEL_NAIVE) {
             const Slab &s = h->slabs[0];
-            cudaEvent_t e0 = nullptr, e1 = nullptr;
-            if (h->prof) {
-                e0 = prof_event(h);
-                e1 = prof_event(h);
-                CK(cudaEventRecord(e0, h->stream));
-            }
+            heat1d_s::ProfRec rec;
+            int rc = prof_begin(h, h->stream, &rec, 0, HEAT1D_TRACE_K1);
+            if (rc) return rc;
             // one step per launch: matched mode runs the oracle's literal sequence (OPS 5), fast
             // mode the contracted 3-op form
             CK(heat1d::launch_naive(h->mode == HEAT1D_MODE_MATCHED ? 5 : 3, cell0(h, s, h->cur),
                                     cell0(h, s, h->cur ^ 1), s.count, h->r, h->stream));
-            if (h->prof) CK(cudaEventRecord(e1, h->stream));
+            rc = prof_end(h, h->stream, rec);
+            if (rc) return rc;
             h->launches++;
             h->cur ^= 1;
             done += 1;
@@ -407,6 +440,9 @@ int run_passes(heat1d_t h, int64_t nt) {
             // B[T, n-T), K3 writes B[0,T) and B[n-T, n): disjoint; both read A.
             CK(cudaEventRecord(h->ev_ready, h->stream));
             CK(cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
+            heat1d_s::ProfRec crec;
+            int prc = prof_begin(h, h->comm, &crec, 1, HEAT1D_TRACE_HALO);
+            if (prc) return prc;
             if (const char *dl = getenv("HEAT1D_COMM_DELAY_US")) {  // fault injection (tests)
                 CK(heat1d::launch_delay((unsigned)atoi(dl), h->comm));
                 h->launches++;
@@ -442,6 +478,8 @@ int run_passes(heat1d_t h, int64_t nt) {
                     h->launches++;
                 }
             }
+            prc = prof_end(h, h->comm, crec);
+            if (prc) return prc;
             CK(cudaEventRecord(h->ev_halo, h->comm));
             for (const Slab &s : h->slabs) {
                 rc = launch_pass_slab(h, s, Tp, Tp, s.count - Tp, 0);
@@ -1520,6 +1558,11 @@ int heat1d_set_profiling(heat1d_t h, int on) {
     h->prof = on != 0;
     h->prof_ms = 0.0;
     h->prof_launches = 0;
+    h->trace.clear();
+    if (h->prof) {
+        if (!h->prof_t0) CK(cudaEventCreate(&h->prof_t0));
+        CK(cudaEventRecord(h->prof_t0, h->stream));
+    }
     return HEAT1D_OK;
 }
 
@@ -1530,6 +1573,18 @@ int heat1d_profile(heat1d_t h, int64_t *launches, double *ms) {
     if (rc) return rc;
     if (launches) *launches = h->prof_launches;
     if (ms) *ms = h->prof_ms;
+    return HEAT1D_OK;
+}
+
+int heat1d_trace(heat1d_t h, heat1d_trace_event *events, int64_t cap, int64_t *count) {
+    int rc = guard(h);
+    if (rc) return rc;
+    if (!count || (cap > 0 && !events)) return set_error(h, HEAT1D_EINVAL, "trace: NULL output");
+    rc = prof_collect(h);
+    if (rc) return rc;
+    const int64_t n = (int64_t)h->trace.size();
+    for (int64_t i = 0; i < n && i < cap; ++i) events[i] = h->trace[(size_t)i];
+    *count = n;
     return HEAT1D_OK;
 }
 
@@ -1568,7 +1623,8 @@ int heat1d_destroy(heat1d_t h) {
     }
     if (h->nccl) ncclCommDestroy(h->nccl);
     for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);
-    for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->ev_all) cudaEventDestroy(e);
+    if (h->prof_t0) cudaEventDestroy(h->prof_t0);
     if (h->ev_ready) cudaEventDestroy(h->ev_ready);
     if (h->ev_halo) cudaEventDestroy(h->ev_halo);
     if (h->own_comm && h->comm) cudaStreamDestroy(h->comm);

@@ -92,6 +92,14 @@ class Info(ctypes.Structure):
     ]
 
 
+class TraceEvent(ctypes.Structure):
+    _fields_ = [("stream", ctypes.c_int32), ("kind", ctypes.c_int32), ("t0_ms", ctypes.c_double),
+                ("t1_ms", ctypes.c_double)]
+
+
+TRACE_KINDS = {1: "K1", 2: "K2", 3: "halo", 6: "K6"}
+
+
 class ExchangePlan(ctypes.Structure):
     _fields_ = [
         ("left", ctypes.c_int32),
@@ -111,7 +119,7 @@ EXPORTS = (
     "heat1d_local_range", "heat1d_set_initial", "heat1d_init_uniform", "heat1d_run",
     "heat1d_get", "heat1d_steps_done", "heat1d_info", "heat1d_set_profiling",
     "heat1d_profile", "heat1d_stream", "heat1d_destroy", "heat1d_last_error", "heat1d_solve_host",
-    "heat1d_solve_host_halo",
+    "heat1d_solve_host_halo", "heat1d_trace",
 )
 
 _lib = None
@@ -154,6 +162,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "heat1d_set_profiling": (ctypes.c_int, [H, ctypes.c_int]),
         "heat1d_profile": (ctypes.c_int, [H, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double)]),
         "heat1d_stream": (vp, [H]),
+        "heat1d_trace": (ctypes.c_int, [H, ctypes.POINTER(TraceEvent), i64, ctypes.POINTER(i64)]),
         "heat1d_destroy": (ctypes.c_int, [H]),
         "heat1d_last_error": (ctypes.c_char_p, [H]),
     }
@@ -364,6 +373,14 @@ class Heat1D:
         n, ms = ctypes.c_int64(), ctypes.c_double()
         _check(self._lib.heat1d_profile(self._h, ctypes.byref(n), ctypes.byref(ms)), self._h)
         return n.value, ms.value
+
+    def trace(self):
+        """[(stream, kind, t0_ms, t1_ms), ...] of the profiling session (heat1d_trace)."""
+        n = ctypes.c_int64()
+        _check(self._lib.heat1d_trace(self._h, None, 0, ctypes.byref(n)), self._h)
+        buf = (TraceEvent * max(1, n.value))()
+        _check(self._lib.heat1d_trace(self._h, buf, n.value, ctypes.byref(n)), self._h)
+        return [(e.stream, TRACE_KINDS.get(e.kind, str(e.kind)), e.t0_ms, e.t1_ms) for e in buf[:n.value]]
 
 
 def _stream_ptr(s) -> Optional[int]:
