@@ -1,7 +1,9 @@
 #!/usr/bin/env python
 """Time variant builds (tools/ab_build.py) on the same workloads, one process per variant.
 
-    python tools/ab_time.py --variants base noguard --N 268435456 --nt 384 --cases 0.5:matched 0.4:matched
+    python tools/ab_time.py --variants base noguard --N 268435456 --nt 384 --cases 0.5:matched 0.4:matched:64:51,4,2,2,3
+
+A case is k:mode[:T[:geometry]] (geometry = HEAT1D_GEOM "V,NW,S,ctas,kind").
 
 Prints one JSON line per (variant, case): best-of-reps GLUPS of heat1d_run (CUDA events).
 """
@@ -20,10 +22,15 @@ import paper_2307_01117_b200 as h1
 torch.cuda.set_device(0)
 st = torch.cuda.current_stream()
 for case in %(cases)r:
-    k, mode = case.split(":")[:2]
-    T = int(case.split(":")[2]) if case.count(":") >= 2 else 0
-    k = float(k)
-    with h1.Heat1D(%(N)d, 1, %(nt)d, k, 1.0, 1.0, T=T, mode=mode, stream=st, resident=%(resident)s,
+    parts = case.split(":")
+    k, mode = float(parts[0]), parts[1]
+    T = int(parts[2]) if len(parts) > 2 and parts[2] else 0
+    if len(parts) > 3 and parts[3]:
+        os.environ["HEAT1D_GEOM"] = parts[3]   # read at create
+    else:
+        os.environ.pop("HEAT1D_GEOM", None)
+    try:
+      with h1.Heat1D(%(N)d, 1, %(nt)d, k, 1.0, 1.0, T=T, mode=mode, stream=st, resident=%(resident)s,
                    virtual_slabs=%(vs)d) as h:
         h.init_uniform(1234, -1.0, 1.0)
         h.run(%(nt)d)
@@ -33,7 +40,11 @@ for case in %(cases)r:
             e0.record(st); h.run(%(nt)d); e1.record(st); torch.cuda.synchronize()
             best = min(best, e0.elapsed_time(e1))
         info = h.info()
+    except Exception as ex:
+        print(json.dumps({"variant": %(name)r, "case": case, "error": str(ex)[:100]}), flush=True)
+        continue
     print(json.dumps({"variant": %(name)r, "case": case, "T": info["T"], "ops": info["dp_ops"],
+                      "geom": "%%d,%%d,%%d,k%%d" %% (info["pass_V"], info["pass_NW"], info["pass_S"], info["pass_kind"]),
                       "glups": round(%(N)d * %(nt)d / (best / 1e3) / 1e9, 1), "ms": round(best, 3)}), flush=True)
 '''
 
