@@ -391,9 +391,11 @@ def step_stats(per, updates_per_step):
 def measure(h1, cfg, mode, args, world, rank, local_rank, stream, u0_dev, with_e2e, sampler_on):
     """Time K steps (after W warm-ups) of one full solve in `mode`; max over ranks."""
     import torch
+    # non-blocking handle: set_initial/run/get are stream-ordered (no host synchronisation between
+    # the steps; the timed region is bracketed by synchronize + CUDA events on that stream)
     h = h1.Heat1D(cfg.nx, cfg.np, cfg.nt, cfg.k, cfg.dt, cfg.dx, T=args.T, mode=mode, rank=rank,
                   nranks=world, nccl_id=fresh_nccl_id(h1, world, rank), device=local_rank, stream=stream,
-                  virtual_slabs=args.virtual_slabs, transport=args.transport)
+                  virtual_slabs=args.virtual_slabs, transport=args.transport, blocking=False)
     first, count = h.local_range
 
     def step():
@@ -526,7 +528,10 @@ def main():
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    stream = torch.cuda.current_stream()
+    # a real stream (torch's default stream has handle 0, which the C ABI reads as "create
+    # your own"): the handles, the timing events and torch's own copies all run on it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
 
     # device-resident u0 for this rank's slab (inputs in HBM before the timed region)
     first, count = h1.partition(cfg.nx, cfg.np, world, rank)

@@ -96,8 +96,11 @@ typedef struct {
                                ONE device that exchange halos by device copies -- the exact
                                multi-GPU schedule with the transport replaced (test harness) */
     int32_t kernel;         /* HEAT1D_KERNEL_*                                              */
-    int32_t blocking;       /* nonzero (default): heat1d_run returns after the device is done;
-                               zero: heat1d_run only enqueues on `stream`                   */
+    int32_t blocking;       /* nonzero (default): heat1d_set_initial / heat1d_run / heat1d_get
+                               return after the device is done; zero: they only enqueue on
+                               `stream` (stream-ordered: keep u0 intact and read `out` only
+                               after synchronising the stream; fast mode's max|u0| check in
+                               set_initial still synchronises)                               */
     int32_t use_graphs;     /* nonzero (default): replay pass sequences as CUDA graphs      */
     int32_t resident;       /* -1 (default) auto, 0 never, 1 required: solve a ring that fits
                                on chip (single slab, single rank, <= ~1.8 M cells) in ONE
@@ -212,7 +215,8 @@ HEAT1D_API int heat1d_local_range(heat1d_t h, int64_t *first, int64_t *count);
 
 /* The initial condition u(0, x_i) of this rank's slab (P:71 gives u(0, x_i) = x_i; any
  * values are accepted).  u0: `count` (= the local slab) fp64 values, host or device
- * pointer, COPIED before return (the caller may free u0 at once; the caller owns it).
+ * pointer, COPIED before return (the caller may free u0 at once; the caller owns it) --
+ * on a non-blocking handle (opts.blocking = 0) the copy is only enqueued on the stream.
  * Resets steps_done to 0; in fast mode checks max|u0| (K5, DESIGN.md c21).
  * EINVAL: NULL u0 or count != local count.  EUNSUPPORTED on a streaming handle. */
 HEAT1D_API int heat1d_set_initial(heat1d_t h, const double *u0, int64_t count);
@@ -233,7 +237,8 @@ HEAT1D_API int heat1d_init_uniform(heat1d_t h, uint64_t seed, double lo, double 
 HEAT1D_API int heat1d_run(heat1d_t h, int64_t nt);
 
 /* Copy this slab's current state u(t, x_i) (t = steps_done) to out: `count` (= the local
- * slab) fp64, host or device pointer, caller-owned; synchronous.  EINVAL: NULL out or
+ * slab) fp64, host or device pointer, caller-owned; synchronous (non-blocking handles:
+ * enqueued on the stream).  EINVAL: NULL out or
  * count mismatch.  ESTATE before an initial state. */
 HEAT1D_API int heat1d_get(heat1d_t h, double *out, int64_t count);
 

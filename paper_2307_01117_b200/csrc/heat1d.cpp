@@ -1192,7 +1192,9 @@ static int after_initial(heat1d_t h) {
     }
     int rc = select_fast_ops(h);
     if (rc) return rc;
-    CK(cudaStreamSynchronize(h->stream));
+    // blocking handles return with the copy done (the caller may reuse u0 at once); non-blocking
+    // ones only enqueue it on the stream (fast mode's range check above already synchronised)
+    if (h->blocking) CK(cudaStreamSynchronize(h->stream));
     h->initialized = true;
     h->steps_done = 0;
     return HEAT1D_OK;
@@ -1266,7 +1268,7 @@ int heat1d_get(heat1d_t h, double *out, int64_t count) {
         CK(cudaMemcpyAsync(out + off, cell0(h, s, h->cur), (size_t)s.count * 8, cudaMemcpyDefault, h->stream));
         off += s.count;
     }
-    CK(cudaStreamSynchronize(h->stream));
+    if (h->blocking) CK(cudaStreamSynchronize(h->stream));
     return HEAT1D_OK;
 }
 
@@ -1471,6 +1473,7 @@ int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, d
         rc = heat1d_set_initial(h, u0, count);
         if (!rc) rc = heat1d_run(h, nt);
         if (!rc) rc = heat1d_get(h, out, count);
+        if (!rc && !h->blocking) CK(cudaStreamSynchronize(h->stream));  // out is filled on return
         return rc;
     }
     if (h->nranks == 1)  // one slab = the whole ring: the halos are its own ends (periodic wrap)

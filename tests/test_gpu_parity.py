@@ -861,3 +861,33 @@ def test_solve_host_halo_emulates_ranks(h1, G, mode):
         with pytest.raises(h1.Heat1DError) as ei:
             h.solve_host_halo(u0[:1000].copy(), u0[:100].copy(), u0[:100].copy(), 100)
         assert ei.value.status == 7
+
+
+@pytest.mark.parametrize("resident", [True, False])
+def test_non_blocking_handle_is_stream_ordered(h1, resident):
+    """opts.blocking = 0: set_initial / run / get only enqueue on the handle's stream; after a
+    stream synchronisation the result equals the oracle bitwise (device and pinned host buffers)."""
+    import torch
+    N, nt = 300_007, 130
+    u0 = synth.uniform(71, 0, N, -1.0, 1.0)
+    want = oracle.run(u0, 0.5, nt)
+    st = torch.cuda.Stream()
+    torch.cuda.set_stream(st)  # torch's copies below are ordered with the handle's work
+    with h1.Heat1D(N, 1, nt, 0.5, 1.0, 1.0, blocking=False, stream=st, resident=resident) as h:
+        dev_in = torch.from_numpy(u0).cuda()
+        dev_out = torch.empty_like(dev_in)
+        for _ in range(2):
+            h.set_initial(dev_in)
+            h.run(nt)
+            h.get(dev_out)
+        torch.cuda.synchronize()
+        assert_bitwise(dev_out.cpu().numpy(), want, "non-blocking, device buffers")
+        host_in = torch.from_numpy(u0).pin_memory()
+        host_out = torch.empty(N, dtype=torch.float64).pin_memory()
+        h.set_initial(host_in)
+        h.run(nt)
+        h.get(host_out)
+        torch.cuda.synchronize()
+        assert_bitwise(host_out.numpy(), want, "non-blocking, pinned host buffers")
+        assert_bitwise(h.solve_host(u0, nt), want, "non-blocking handle, solve_host returns filled")
+    torch.cuda.set_stream(torch.cuda.default_stream())
