@@ -1,0 +1,162 @@
+"""CPU pins of the exactness guard's theory (reading c3, stencil.cuh).  -m "not gpu".
+
+The GPU's matched mode evaluates Eq. 2 with contracted forms:
+
+    OPS_FMA3 (r = 2^-j):  t = fma(-2, b, a);  t = t + c;  u' = fma(r, t, b)
+
+and runs the oracle's literal sequence (2.0*b, a - ., + c, r * ., b + .) for any block of Tp
+steps whose input cells fail the guard:
+
+    top:    |x| < 2^1022                         (r <= 1/2)
+    bottom: x == 0  or  |x| >= 2^(j*Tp - 1022)
+
+The claim: a block whose input cells all pass gives, after every one of its Tp steps, exactly
+the literal sequence's values.  These tests check it with an independent emulation: fma(x, y, z)
+is evaluated exactly with `fractions` and rounded once (Python's int/int true division is
+correctly rounded, subnormals included), the literal sequence is the C oracle itself.  Rings are
+small (Python speed); magnitudes straddle both bounds.  Also pinned: the guard is not vacuous --
+the known counterexamples (SURVEY r1 / VERDICT r1) fail it and do differ.
+"""
+from __future__ import annotations
+
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+
+def fma(x: float, y: float, z: float) -> float:
+    """Correctly rounded x*y + z (one rounding), IEEE binary64 incl. subnormals and overflow."""
+    if not (math.isfinite(x) and math.isfinite(y) and math.isfinite(z)):
+        return x * y + z  # inf/NaN operands: the same IEEE result either way
+    exact = Fraction(x) * Fraction(y) + Fraction(z)
+    if exact == 0:
+        if (x == 0 or y == 0) and z == 0:  # a sum of two zeros: -0 only if both are -0
+            return math.copysign(0.0, math.copysign(1.0, x) * math.copysign(1.0, y)) + z
+        return 0.0                         # exact cancellation: +0 under round-to-nearest
+    try:
+        return exact.numerator / exact.denominator
+    except OverflowError:                  # beyond the largest finite value: rounds to inf
+        return math.inf if exact > 0 else -math.inf
+
+
+def step_fma3(u: np.ndarray, r: float) -> np.ndarray:
+    """One Jacobi step of the contracted 3-op form on a periodic ring (the GPU's OPS_FMA3)."""
+    n = u.size
+    out = np.empty_like(u)
+    for i in range(n):
+        a, b, c = float(u[(i - 1) % n]), float(u[i]), float(u[(i + 1) % n])
+        t = fma(-2.0, b, a)
+        t = t + c
+        out[i] = fma(r, t, b)
+    return out
+
+
+def guard_passes(u: np.ndarray, r: float, Tp: int) -> bool:
+    """The guard of stencil.cuh for the 3-op form and r = 2^-j <= 1/2, restated from the theory."""
+    j = -int(round(math.log2(r)))
+    bottom = math.ldexp(1.0, j * Tp - 1022)
+    a = np.abs(u)
+    return bool(np.all(a < math.ldexp(1.0, 1022)) and np.all((u == 0) | (a >= bottom)))
+
+
+def ring(seed: int, n: int, exp_lo: int, exp_hi: int, zeros: float = 0.0) -> np.ndarray:
+    """Seeded values m * 2^e, |m| < 2^53, e uniform in [exp_lo, exp_hi]; some exact zeros."""
+    m = np.floor(synth.uniform(seed, 0, n, -(2.0 ** 53), 2.0 ** 53))
+    e = np.floor(synth.uniform(seed + 1, 0, n, exp_lo, exp_hi + 1)).astype(np.int64)
+    u = np.ldexp(m, e - 52)
+    if zeros:
+        u[synth.uniform(seed + 2, 0, n) < zeros] = 0.0
+    return u
+
+
+def test_exact_fma_emulation_against_known_values():
+    """The emulation itself: hand values, a double rounding it must avoid, subnormal ties."""
+    assert fma(2.0, 3.0, 1.0) == 7.0
+    # x*y + z with x*y not representable: one rounding of the exact sum
+    x = 1.0 + 2.0 ** -30
+    assert fma(x, x, -1.0) == 2.0 ** -29 + 2.0 ** -60      # exact; the separate product would round away 2^-60
+    assert (x * x) - 1.0 == 2.0 ** -29                       # the two-rounding result differs
+    u = 2.0 ** -1074
+    assert fma(0.5, 7 * u, 1 * u) == 4 * u                   # 4.5u -> ties to even
+    assert 1 * u + 0.5 * (7 * u) == 5 * u                    # the literal order: 3.5u -> 4u, then 5u
+
+
+@pytest.mark.parametrize("r", [0.5, 0.25])
+def test_known_counterexamples_fail_the_guard_and_differ(r):
+    """Where the contracted form is NOT exact, the guard must reject the block."""
+    u = 2.0 ** -1074
+    if r == 0.5:   # cell 1: t = 7u; literal 1u + fl(3.5u) = 1u + 4u = 5u; fma: fl(4.5u) = 4u
+        u0 = np.array([4 * u, 1 * u, 5 * u])
+    else:          # cell 1: t = 10u; literal 1u + fl(2.5u) = 1u + 2u = 3u; fma: fl(3.5u) = 4u
+        u0 = np.array([6 * u, 1 * u, 6 * u])
+    lit = oracle.run(u0, r, 1)
+    f3 = step_fma3(u0, r)
+    assert lit[1] != f3[1], "the example should expose the contraction"
+    assert not guard_passes(u0, r, 1)
+    # 2b overflow: b = 2^1023, the oracle's 2.0*b is inf (cell 1 -> -inf); fma(-2, b, a) is the
+    # finite a - 2b = -2^1021
+    big = np.array([1.75 * 2.0 ** 1023, 2.0 ** 1023, 1.0])
+    lit, f3 = oracle.run(big, 0.5, 1), step_fma3(big, 0.5)
+    assert np.isinf(lit[1]) and np.isfinite(f3[1])
+    assert not guard_passes(big, 0.5, 1)
+
+
+@pytest.mark.parametrize("r,Tp", [(0.5, 4), (0.5, 8), (0.25, 4), (0.125, 3)])
+def test_guard_passing_blocks_equal_the_literal_sequence(r, Tp):
+    """Blocks that pass the guard: the 3-op form equals the oracle after EVERY step of the block.
+    Magnitudes straddle the bottom bound 2^(j*Tp - 1022) (some blocks pass, some fail), with exact
+    zeros mixed in; rings of 24 cells, 40 seeded blocks per case."""
+    j = -int(round(math.log2(r)))
+    lo_exp = j * Tp - 1022
+    passed = 0
+    for seed in range(40):
+        u0 = ring(1000 * Tp + seed, 24, lo_exp - 3, lo_exp + 60, zeros=0.15)
+        if not guard_passes(u0, r, Tp):
+            continue
+        passed += 1
+        lit, f3 = u0.copy(), u0.copy()
+        for s in range(Tp):
+            lit = oracle.run(lit, r, 1)
+            f3 = step_fma3(f3, r)
+            assert np.array_equal(lit.view(np.uint64), f3.view(np.uint64)), (seed, s)
+    assert passed >= 5, "too few passing blocks to pin anything"
+
+
+def test_bound_is_tight_enough_to_matter():
+    """Just below the bottom bound the contracted form can differ within the block: search a few
+    seeded rings one step of j*Tp below the bound and find a step where fma3 != literal (so the
+    bound is not needlessly loose in the other direction either)."""
+    r, Tp = 0.5, 6
+    found = False
+    for seed in range(200):
+        u0 = ring(77_000 + seed, 16, -1074 + 52, -1074 + 52 + 3)  # tiny normals/subnormal-range magnitudes
+        if guard_passes(u0, r, Tp):
+            continue
+        lit, f3 = u0.copy(), u0.copy()
+        for _ in range(Tp):
+            lit = oracle.run(lit, r, 1)
+            f3 = step_fma3(f3, r)
+            if not np.array_equal(lit.view(np.uint64), f3.view(np.uint64)):
+                found = True
+                break
+        if found:
+            break
+    assert found
+
+
+def test_top_bound_blocks_equal_the_literal_sequence():
+    """|x| just below 2^1022: no overflow of 2b anywhere in the block; equal to the oracle."""
+    r, Tp = 0.5, 5
+    for seed in range(10):
+        u0 = ring(5000 + seed, 20, 1000, 1021)
+        assert guard_passes(u0, r, Tp)
+        lit, f3 = u0.copy(), u0.copy()
+        for _ in range(Tp):
+            lit = oracle.run(lit, r, 1)
+            f3 = step_fma3(f3, r)
+        assert np.array_equal(lit.view(np.uint64), f3.view(np.uint64))
