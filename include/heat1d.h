@@ -99,8 +99,7 @@ typedef struct {
     int32_t blocking;       /* nonzero (default): heat1d_set_initial / heat1d_run / heat1d_get
                                return after the device is done; zero: they only enqueue on
                                `stream` (stream-ordered: keep u0 intact and read `out` only
-                               after synchronising the stream; fast mode's max|u0| check in
-                               set_initial still synchronises)                               */
+                               after synchronising the stream)                              */
     int32_t use_graphs;     /* nonzero (default): replay pass sequences as CUDA graphs      */
     int32_t resident;       /* -1 (default) auto, 0 never, 1 required: solve a ring that fits
                                on chip (single slab, single rank, <= ~1.8 M cells) in ONE
@@ -217,7 +216,8 @@ HEAT1D_API int heat1d_local_range(heat1d_t h, int64_t *first, int64_t *count);
  * values are accepted).  u0: `count` (= the local slab) fp64 values, host or device
  * pointer, COPIED before return (the caller may free u0 at once; the caller owns it) --
  * on a non-blocking handle (opts.blocking = 0) the copy is only enqueued on the stream.
- * Resets steps_done to 0; in fast mode checks max|u0| (K5, DESIGN.md c21).
+ * Resets steps_done to 0; in fast mode K5 computes max|u0| on the device, where the scaled
+ * kernels read it (DESIGN.md c21; no host round trip).
  * EINVAL: NULL u0 or count != local count.  EUNSUPPORTED on a streaming handle. */
 HEAT1D_API int heat1d_set_initial(heat1d_t h, const double *u0, int64_t count);
 
@@ -255,8 +255,8 @@ HEAT1D_API int heat1d_get(heat1d_t h, double *out, int64_t count);
  * heat1d_plan_exchange at depth nt, NCCL; collective, every rank takes the same branch);
  * otherwise it IS the plain three-call sequence.  u0/out (caller-owned) should be pinned
  * (cudaHostAlloc / torch pin_memory) for the copies to overlap.  In fast mode every
- * window checks its own max|u0| (K5) and is recomputed with the 3-op form if the scaled
- * state could overflow (DESIGN.md c21).  Afterwards the device state is consumed: call
+ * window's own max|u0| (K5) decides on the device whether it runs the scaled form or the
+ * 3-op form (DESIGN.md c21).  Afterwards the device state is consumed: call
  * set_initial before run/get.  EINVAL: NULL or overlapping u0/out, count mismatch.
  * EUNSUPPORTED: a streaming handle whose window cannot hold nt.  Else as run. */
 HEAT1D_API int heat1d_solve_host(heat1d_t h, const double *u0, int64_t count, int64_t nt, double *out);

@@ -189,6 +189,7 @@ int64_t pad_for(int T) { return round_up((int64_t)T + 2, 16); }
 
 // Exactness guard (stencil.cuh, DESIGN.md c3) of a block of Tp steps in arithmetic `ops`.
 heat1d::Guard guard_for(heat1d_t h, int ops, int Tp);
+heat1d::FastRange fast_range(heat1d_t h, int ops, const unsigned long long *word);
 
 // Plain partition arithmetic (also exported as heat1d_partition).
 int partition(int64_t nx, int64_t np, int32_t G, int32_t g, int64_t *first, int64_t *count) {
@@ -331,14 +332,35 @@ heat1d::Guard guard_for(heat1d_t h, int ops, int Tp) {
     return heat1d::guard_of(h->mode == HEAT1D_MODE_MATCHED, ops, h->r, Tp);
 }
 
+// The scaled fast forms' range (DESIGN.md c21): a pass of up to T steps grows the scaled state to
+// max|u0| * r^-T, which must stay below 2^1000, i.e. max|u0| < 2^E with E the largest integer
+// below 1000 - T log2(1/r).  `word` = a K5 max|u| word on the device.
+heat1d::FastRange fast_range(heat1d_t h, int ops, const unsigned long long *word) {
+    heat1d::FastRange f;
+    if (!heat1d::ops_scaled(ops)) return f;
+    const double X = 1000.0 - (double)h->T * std::log2(1.0 / h->r);
+    const double E = std::ceil(X) - 1.0;
+    f.absmax = word;
+    f.r = h->r;
+    if (E < -1074.0) {
+        f.limit = 0ull;  // only an all-zero state
+    } else {
+        const double lim = std::ldexp(1.0, (int)E);
+        unsigned long long bits;
+        memcpy(&bits, &lim, sizeof bits);
+        f.limit = bits - 1ull;  // |x| bits <= limit  <=>  |x| < 2^E
+    }
+    return f;
+}
+
 int launch_pass_slab(heat1d_t h, const Slab &s, int Tp, int64_t lo, int64_t hi, int wrapT) {
     heat1d_s::ProfRec rec;
     int rc = prof_begin(h, h->stream, &rec, 0, HEAT1D_TRACE_K2);
     if (rc) return rc;
     int grid = 0;
     CK(heat1d::launch_pass(h->geom, h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp, lo, hi,
-                           wrapT, h->q, heat1d::scale_of(h->r, Tp), guard_for(h, h->ops, Tp), h->num_sms,
-                           h->stream, &grid));
+                           wrapT, h->q, heat1d::scale_of(h->r, Tp), guard_for(h, h->ops, Tp),
+                           fast_range(h, h->ops, h->absmax), h->num_sms, h->stream, &grid));
     if (grid > 0) h->launches++;
     h->last_grid = grid > 0 ? grid : h->last_grid;
     return prof_end(h, h->stream, rec);
@@ -394,8 +416,8 @@ int run_resident(heat1d_t h, int64_t nt) {
         h->k6_base += (unsigned)((nt + h->T - 1) / h->T) + 2u;
     }
     CK(heat1d::launch_resident(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, h->T, nt, h->q,
-                               h->r, guard_for(h, h->ops, h->T), h->res_scratch, h->num_sms, h->stream,
-                               &h->res_warps, mb));
+                               h->r, guard_for(h, h->ops, h->T), fast_range(h, h->ops, h->absmax), h->res_scratch,
+                               h->num_sms, h->stream, &h->res_warps, mb));
     h->launches++;
     rc = prof_end(h, h->stream, rec);
     if (rc) return rc;
@@ -463,7 +485,7 @@ int run_passes(heat1d_t h, int64_t nt) {
                 for (const Slab &s : h->slabs) {
                     CK(heat1d::launch_edges_put(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp,
                                                 h->q, heat1d::scale_of(h->r, Tp), guard_for(h, h->ops, Tp),
-                                                s.flags, h->xg,
+                                                fast_range(h, h->ops, h->absmax), s.flags, h->xg,
                                                 s.put_left[h->cur ^ 1], s.put_right[h->cur ^ 1], s.nflag_left,
                                                 s.nflag_right, h->comm));
                     h->launches++;
@@ -474,7 +496,8 @@ int run_passes(heat1d_t h, int64_t nt) {
                 if (rc) return rc;
                 for (const Slab &s : h->slabs) {
                     CK(heat1d::launch_edges(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, Tp, h->q,
-                                            heat1d::scale_of(h->r, Tp), guard_for(h, h->ops, Tp), h->comm));
+                                            heat1d::scale_of(h->r, Tp), guard_for(h, h->ops, Tp),
+                                            fast_range(h, h->ops, h->absmax), h->comm));
                     h->launches++;
                 }
             }
@@ -905,11 +928,10 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
         else if (r >= 1.0 / 256.0 && r < 0.5)
             h->ops = 2;
     }
-    if (heat1d::ops_scaled(h->ops)) {
-        h->ops_fast = h->ops;
-        h->ops = 3;  // until set_initial has checked the range of u0 (after_initial)
-    }
-    h->q = r;
+    if (heat1d::ops_scaled(h->ops)) h->ops_fast = h->ops;
+    // the scaled forms' per-step coefficient c = (1-2r)/r; the kernels fall back to the 3-op
+    // form with r themselves when K5 finds max|u0| out of range (FastRange, kernels.h)
+    h->q = heat1d::ops_scaled(h->ops) ? (1.0 - 2.0 * r) / r : r;
     auto bail = [&](int rc) {
         heat1d_destroy(h);
         return rc;
@@ -1147,30 +1169,16 @@ int heat1d_local_range(heat1d_t h, int64_t *first, int64_t *count) {
     return HEAT1D_OK;
 }
 
-// Fast mode: the scaled state of a pass reaches at most max|u0| * r^-T (max
-// principle, r <= 1/2).  Use the scaled variant only while that stays below
-// 2^1000 (checked by K5 on every new initial state), else the 3-op form.
-static int select_fast_ops(heat1d_t h) {
+// Fast mode: the scaled state of a pass reaches at most max|u0| * r^-T (max principle,
+// r <= 1/2).  K5 writes max|u0| to a device word; the scaled kernels compare it with their
+// limit themselves (FastRange) and run the 3-op form if it is out of range -- no host round
+// trip, so a non-blocking set_initial only enqueues.
+static int check_fast_range(heat1d_t h) {
     if (!h->ops_fast) return HEAT1D_OK;
     CK(cudaMemsetAsync(h->absmax, 0, sizeof(unsigned long long), h->stream));
     for (const Slab &s : h->slabs) {
         CK(heat1d::launch_absmax(cell0(h, s, h->cur), s.count, h->absmax, h->stream));
         h->launches++;
-    }
-    unsigned long long bits = 0;
-    CK(cudaMemcpyAsync(&bits, h->absmax, sizeof bits, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    double m;
-    memcpy(&m, &bits, sizeof m);
-    int e = 0;
-    if (std::isfinite(m)) std::frexp(m, &e);
-    const bool ok = std::isfinite(m) && (double)e + (double)h->T * std::log2(1.0 / h->r) < 1000.0;
-    const int want = ok ? h->ops_fast : 3;
-    if (want != h->ops) {
-        h->ops = want;
-        h->q = heat1d::ops_scaled(want) ? (1.0 - 2.0 * h->r) / h->r : h->r;
-        for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);  // they bake in the variant
-        h->graphs.clear();
     }
     return HEAT1D_OK;
 }
@@ -1190,10 +1198,10 @@ static int after_initial(heat1d_t h) {
         CK(heat1d::launch_wrap_fill(cell0(h, s, h->cur), s.count, h->pad, h->stream));
         h->launches++;
     }
-    int rc = select_fast_ops(h);
+    int rc = check_fast_range(h);
     if (rc) return rc;
     // blocking handles return with the copy done (the caller may reuse u0 at once); non-blocking
-    // ones only enqueue it on the stream (fast mode's range check above already synchronised)
+    // ones only enqueue it on the stream
     if (h->blocking) CK(cudaStreamSynchronize(h->stream));
     h->initialized = true;
     h->steps_done = 0;
@@ -1305,7 +1313,8 @@ int copy_window_in(heat1d_t h, double *dst, const double *u0, const double *left
 
 // nt steps of one light-cone window X[0, Lw) on the compute stream (ping-pong with Y);
 // pass p writes only the cells still inside the cone.  Returns the result buffer.
-int solve_window(heat1d_t h, int ops, double *X, double *Y, int64_t Lw, int64_t nt, double **res) {
+int solve_window(heat1d_t h, int ops, double *X, double *Y, int64_t Lw, int64_t nt, double **res,
+                 const unsigned long long *range_word) {
     const double q = heat1d::ops_scaled(ops) ? (1.0 - 2.0 * h->r) / h->r : h->r;
     double *a = X, *b = Y;
     int64_t done = 0;
@@ -1313,7 +1322,8 @@ int solve_window(heat1d_t h, int ops, double *X, double *Y, int64_t Lw, int64_t 
         const int Tp = (int)std::min<int64_t>(h->T, nt - done);
         int grid = 0;
         CK(heat1d::launch_pass(h->geom, ops, a, b, Lw, Tp, done + Tp, Lw - done - Tp, 0, q,
-                               heat1d::scale_of(h->r, Tp), guard_for(h, ops, Tp), h->num_sms, h->stream, &grid));
+                               heat1d::scale_of(h->r, Tp), guard_for(h, ops, Tp), fast_range(h, ops, range_word),
+                               h->num_sms, h->stream, &grid));
         h->launches++;
         std::swap(a, b);
         done += Tp;
@@ -1342,14 +1352,6 @@ int ensure_stream_objects(heat1d_t h, int64_t nwin) {
 
 constexpr int kWinSlots = 3;  // light-cone window slots per ping-pong buffer (heat1d_solve_host)
 
-bool fast_range_ok(heat1d_t h, unsigned long long bits) {
-    double m;
-    memcpy(&m, &bits, sizeof m);
-    int e = 0;
-    if (std::isfinite(m)) std::frexp(m, &e);
-    return std::isfinite(m) && (double)e + (double)h->T * std::log2(1.0 / h->r) < 1000.0;
-}
-
 // Window plan: C chunks of L cells, windows of L + 2H cells (H = nt), two slots of two
 // ping-pong buffers carved out of the handle's two ring buffers.  false = not worth it.
 bool stream_plan(heat1d_t h, int64_t nt, int64_t *C, int64_t *L, int64_t *half) {
@@ -1377,7 +1379,7 @@ int solve_windows(heat1d_t h, const double *u0, const double *left, const double
     if (rc) return rc;
     const Slab &s = h->slabs[0];
     const int64_t n = s.count;
-    const int ops = h->ops_fast ? h->ops_fast : h->ops;  // optimistic; checked per window below
+    const int ops = h->ops;  // (scaled fast forms check each window's own max|u0|: FastRange)
     // three window slots: the H2D of window c+1, the compute of window c and the D2H of
     // window c-1 each own one, so the three run fully concurrently (two slots serialise
     // a D2H before the next H2D into the same slot)
@@ -1403,7 +1405,7 @@ int solve_windows(heat1d_t h, const double *u0, const double *left, const double
             h->launches++;
         }
         double *res = nullptr;
-        rc = solve_window(h, ops, X[sl], Y[sl], Lw, nt, &res);
+        rc = solve_window(h, ops, X[sl], Y[sl], Lw, nt, &res, h->ops_fast ? h->win_absmax + c : nullptr);
         if (rc) return rc;
         CK(cudaEventRecord(h->ev_comp[sl], h->stream));
         CK(cudaStreamWaitEvent(h->st_d2h, h->ev_comp[sl], 0));
@@ -1413,23 +1415,6 @@ int solve_windows(heat1d_t h, const double *u0, const double *left, const double
     CK(cudaStreamSynchronize(h->st_h2d));
     CK(cudaStreamSynchronize(h->stream));
     CK(cudaStreamSynchronize(h->st_d2h));
-    if (h->ops_fast) {  // rare: a window whose scaled state could overflow -> redo with 3 ops
-        std::vector<unsigned long long> bits((size_t)C);
-        CK(cudaMemcpy(bits.data(), h->win_absmax, (size_t)C * 8, cudaMemcpyDeviceToHost));
-        for (int64_t c = 0; c < C; ++c) {
-            if (fast_range_ok(h, bits[(size_t)c])) continue;
-            const int64_t a = c * L, len = std::min(L, n - a), Lw = len + 2 * nt;
-            rc = copy_window_in(h, X[0], u0, left, right, nt, n, a - nt, Lw);
-            if (rc) return rc;
-            CK(cudaEventRecord(h->ev_in[0], h->st_h2d));
-            CK(cudaStreamWaitEvent(h->stream, h->ev_in[0], 0));
-            double *res = nullptr;
-            rc = solve_window(h, 3, X[0], Y[0], Lw, nt, &res);
-            if (rc) return rc;
-            CK(cudaMemcpyAsync(out + a, res + nt, (size_t)len * 8, cudaMemcpyDefault, h->stream));
-            CK(cudaStreamSynchronize(h->stream));
-        }
-    }
     h->steps_done = nt;
     h->stream_windows = C;
     return HEAT1D_OK;

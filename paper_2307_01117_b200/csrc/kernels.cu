@@ -244,7 +244,8 @@ __device__ __forceinline__ void write_back(const double (&u)[V], double *st, int
 }
 
 // The guard's fallback (rare): a tile with the literal 5-op sequence.  Out of line, so
-// its registers do not add to the hot path's.
+// its registers do not add to the hot path's.  (Measured: an inline copy of the tile loop
+// for the rest of the pass after a failing tile instead cost 2.5 % -- the code size.)
 template <int V, int NW, int KX>
 __device__ __noinline__ void tile_literal(double *st, int base, int T, double r, double *xbuf, int warp, int lane) {
     double u[V];
@@ -254,13 +255,39 @@ __device__ __noinline__ void tile_literal(double *st, int base, int T, double r,
     write_back<V, NW, KX>(u, st, base, T, warp, lane);
 }
 
+// The compute warps' tile loop in the contracted 3-op form (coefficient r): fast mode's
+// fallback for a pass whose scaled state could overflow (FastRange).  Inlined as a disjoint
+// branch: a call (out of line) would constrain the hot loop's registers (-2 %).
+template <int V, int NW, int S, int KX>
+__device__ __forceinline__ void compute_loop_fma3(uint64_t *full, uint64_t *done, double *stages,
+                                               uint32_t stage_doubles, int64_t out_lo, int64_t W, int T, double r,
+                                               int64_t ntiles, double *xbuf, int warp, int lane) {
+    const int SW = 32 * V - 2 * KX;
+    int k = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+        const int s = k % S;
+        double *st = stages + (size_t)s * stage_doubles;
+        const int64_t x0 = out_lo + tile * W;
+        mbar_wait_sleep(&full[s], (uint32_t)((k / S) & 1));
+        const int base = (int)((x0 - T) & 1) + warp * SW + lane * V;
+        double u[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) u[j] = st[base + j];
+        tile_steps<V, NW, KX, 3, false>(u, T, r, 1.0, xbuf, warp, lane, true);
+        write_back<V, NW, KX>(u, st, base, T, warp, lane);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&done[s]);
+    }
+}
+
 // Register target: the occupancy choose_geom plans for (2 CTAs/SM; 4 for V <= 17 tiles).
 // Without it ptxas sizes the kernel for the guard's out-of-line fallback as well.
 template <int V, int NW, int S, int OPS, int KX>
 __global__ void __launch_bounds__((NW + 1) * 32, V <= 17 ? 4 : 2)
 k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t out_lo,
          int64_t out_hi, int wrapT, double r, double scale, int64_t ntiles, uint32_t stage_doubles,
-         Guard guard) {
+         Guard guard, FastRange fr) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);  // TMA landed
     uint64_t *done = full + S;                                 // compute warps finished
@@ -343,6 +370,16 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
     }
 
     // ---------------- compute warps
+    // scaled fast forms whose state could overflow run the whole pass in the 3-op form, in a
+    // separate copy of this loop (no branch inside the hot loop below); the decision is
+    // CTA-uniform, broadcast so that ptxas sees it warp-uniform
+    if constexpr (ops_scaled(OPS)) {
+        if (!__shfl_sync(0xffffffffu, (int)scaled_in_range(fr), 0)) {
+            compute_loop_fma3<V, NW, S, KX>(full, done, stages, stage_doubles, out_lo, W, T, fr.r, ntiles, xbuf,
+                                            warp, lane);
+            return;
+        }
+    }
     int k = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += stride, ++k) {
         const int s = k % S;
@@ -382,7 +419,7 @@ size_t PassGeom::smem_bytes(int T) const {
 namespace {
 
 using PassFn = void (*)(const double *, double *, int64_t, int, int64_t, int64_t, int, double, double,
-                        int64_t, uint32_t, Guard);
+                        int64_t, uint32_t, Guard, FastRange);
 
 // (V, NW, S) instantiated for kinds 3 and 4 and all four arithmetic variants: the
 // two defaults of choose_geom (51,4,2) and (17,4,3) plus the tuning points of the
@@ -433,7 +470,7 @@ PassGeom choose_geom(int64_t n_out, int T, int num_sms, int ops) {
 
 cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, int64_t n, int T,
                         int64_t out_lo, int64_t out_hi, int wrapT, double q, double scale, Guard guard,
-                        int num_sms, cudaStream_t st, int *grid_out) {
+                        const FastRange &fr, int num_sms, cudaStream_t st, int *grid_out) {
     PassFn fn = lookup_pass(g.V, g.NW, g.S, ops, g.kind);
     if (!fn) return cudaErrorInvalidConfiguration;
     if (out_hi <= out_lo) {
@@ -480,7 +517,7 @@ cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, 
     if (grid > units) grid = units;
     if (grid_out) *grid_out = (int)grid;
     fn<<<(unsigned)grid, threads, smem, st>>>(A, B, n, T, out_lo, out_hi, wrapT, q, scale, units, stage_doubles,
-                                             guard);
+                                             guard, fr);
     return cudaGetLastError();
 }
 
@@ -526,40 +563,50 @@ __device__ __forceinline__ int strip_steps(double (*w)[3 * 128], int T, double r
     return cur;
 }
 
+// Returns the buffer holding the result; *scaled = whether it is in the scaled state.
 template <int OPS>
-__device__ __forceinline__ int strip_steps_guarded(double (*w)[3 * 128], int T, double r, Guard guard) {
+__device__ __forceinline__ int strip_steps_guarded(double (*w)[3 * 128], int T, double r, Guard guard,
+                                                   const FastRange &fr, bool *scaled) {
+    *scaled = ops_scaled(OPS);
     if constexpr (ops_guarded(OPS)) {
         GuardAcc acc;
         for (int i = threadIdx.x; i < 3 * T; i += blockDim.x) acc.add(w[0][i]);
         if (!__syncthreads_and(acc.ok(guard))) return strip_steps<5>(w, T, r);
+    }
+    if constexpr (ops_scaled(OPS)) {
+        if (!scaled_in_range(fr)) {
+            *scaled = false;
+            return strip_steps<3>(w, T, fr.r);
+        }
     }
     return strip_steps<OPS>(w, T, r);
 }
 
 template <int OPS>
 __global__ void __launch_bounds__(96) k3_edges(const double *__restrict__ A, double *__restrict__ B, int64_t n,
-                                               int T, double r, double scale, Guard guard) {
+                                               int T, double r, double scale, Guard guard, FastRange fr) {
     __shared__ double w[2][3 * 128];
     const int64_t base = (blockIdx.x == 0) ? -(int64_t)T : n - 2 * (int64_t)T;
     const int len = 3 * T;
     for (int i = threadIdx.x; i < len; i += blockDim.x) w[0][i] = A[base + i];
     __syncthreads();
-    const int cur = strip_steps_guarded<OPS>(w, T, r, guard);
+    bool scaled;
+    const int cur = strip_steps_guarded<OPS>(w, T, r, guard, fr, &scaled);
     for (int i = threadIdx.x; i < T; i += blockDim.x) {
         double x = w[cur][T + i];
-        if constexpr (ops_scaled(OPS)) x = __dmul_rn(x, scale);
+        if (scaled) x = __dmul_rn(x, scale);
         B[base + T + i] = x;
     }
 }
 
 cudaError_t launch_edges(int ops, const double *A, double *B, int64_t n, int T, double q, double scale,
-                         Guard guard, cudaStream_t st) {
+                         Guard guard, const FastRange &fr, cudaStream_t st) {
     if (T < 1 || T > 128) return cudaErrorInvalidValue;
     switch (ops) {
-        case 4: k3_edges<4><<<2, 96, 0, st>>>(A, B, n, T, q, scale, guard); break;
-        case 3: k3_edges<3><<<2, 96, 0, st>>>(A, B, n, T, q, scale, guard); break;
-        case 2: k3_edges<2><<<2, 96, 0, st>>>(A, B, n, T, q, scale, guard); break;
-        case 1: k3_edges<1><<<2, 96, 0, st>>>(A, B, n, T, q, scale, guard); break;
+        case 4: k3_edges<4><<<2, 96, 0, st>>>(A, B, n, T, q, scale, guard, fr); break;
+        case 3: k3_edges<3><<<2, 96, 0, st>>>(A, B, n, T, q, scale, guard, fr); break;
+        case 2: k3_edges<2><<<2, 96, 0, st>>>(A, B, n, T, q, scale, guard, fr); break;
+        case 1: k3_edges<1><<<2, 96, 0, st>>>(A, B, n, T, q, scale, guard, fr); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -586,7 +633,7 @@ __device__ __forceinline__ void st_release_sys_u32(unsigned *p, unsigned v) {
 
 template <int OPS>
 __global__ void __launch_bounds__(96) k3_edges_put(const double *__restrict__ A, double *__restrict__ B, int64_t n,
-                                                   int T, double r, double scale, Guard guard,
+                                                   int T, double r, double scale, Guard guard, FastRange fr,
                                                    const unsigned *my_flags, unsigned g, double *put_left,
                                                    double *put_right, unsigned *flag_left, unsigned *flag_right) {
     __shared__ double w[2][3 * 128];
@@ -603,11 +650,12 @@ __global__ void __launch_bounds__(96) k3_edges_put(const double *__restrict__ A,
     const int len = 3 * T;
     for (int i = threadIdx.x; i < len; i += blockDim.x) w[0][i] = __ldcv(A + base + i);  // pads: peer-written
     __syncthreads();
-    const int cur = strip_steps_guarded<OPS>(w, T, r, guard);
+    bool scaled;
+    const int cur = strip_steps_guarded<OPS>(w, T, r, guard, fr, &scaled);
     double *put = side == 0 ? put_left : put_right;
     for (int i = threadIdx.x; i < T; i += blockDim.x) {
         double x = w[cur][T + i];
-        if constexpr (ops_scaled(OPS)) x = __dmul_rn(x, scale);
+        if (scaled) x = __dmul_rn(x, scale);
         B[base + T + i] = x;
         put[i] = x;
     }
@@ -616,10 +664,11 @@ __global__ void __launch_bounds__(96) k3_edges_put(const double *__restrict__ A,
 }
 
 cudaError_t launch_edges_put(int ops, const double *A, double *B, int64_t n, int T, double q, double scale,
-                             Guard guard, const unsigned *my_flags, unsigned g, double *put_left,
-                             double *put_right, unsigned *flag_left, unsigned *flag_right, cudaStream_t st) {
+                             Guard guard, const FastRange &fr, const unsigned *my_flags, unsigned g,
+                             double *put_left, double *put_right, unsigned *flag_left, unsigned *flag_right,
+                             cudaStream_t st) {
     if (T < 1 || T > 128 || n < 2 * (int64_t)T) return cudaErrorInvalidValue;
-#define K3P(o) k3_edges_put<o><<<2, 96, 0, st>>>(A, B, n, T, q, scale, guard, my_flags, g, put_left, put_right, flag_left, flag_right)
+#define K3P(o) k3_edges_put<o><<<2, 96, 0, st>>>(A, B, n, T, q, scale, guard, fr, my_flags, g, put_left, put_right, flag_left, flag_right)
     switch (ops) {
         case 4: K3P(4); break;
         case 3: K3P(3); break;

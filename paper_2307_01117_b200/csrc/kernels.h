@@ -48,6 +48,17 @@ inline Guard guard_of(bool matched, int ops, double r, int Tp) {
     return g;
 }
 
+// Fast mode's scaled forms (OPS 2, 1; stencil.cuh, DESIGN.md c21) reach max|u0| * r^-T within
+// a pass and must stay below 2^1000: the kernels compare K5's max|u| word (the bit pattern of a
+// non-negative double) with `limit` and, if it is larger, run the contracted 3-op form with the
+// coefficient r instead -- decided on the device, CTA-uniformly, so set_initial needs no host
+// round trip.  absmax == nullptr: always the scaled form.
+struct FastRange {
+    const unsigned long long *absmax = nullptr;
+    unsigned long long limit = ~0ull;
+    double r = 0.0;
+};
+
 // Ghost depth (= steps between exchanges) of the inter-warp exchange of pass-kernel
 // kinds 3 (8) and 4 (16).
 constexpr int kx_of(int kind) { return kind == 3 ? 8 : kind == 4 ? 16 : 0; }
@@ -82,7 +93,7 @@ PassGeom choose_geom(int64_t n_out, int T, int num_sms, int ops);
 // guard = the exactness guard (guard_of; guarded variants only).
 cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, int64_t n,
                         int T, int64_t out_lo, int64_t out_hi, int wrapT, double q, double scale,
-                        Guard guard, int num_sms, cudaStream_t st, int *grid_out);
+                        Guard guard, const FastRange &fr, int num_sms, cudaStream_t st, int *grid_out);
 
 // K1: one step over the whole ring with modular indexing (no pads used); ops 5 (literal,
 // matched mode) or 3 (fast mode).
@@ -90,14 +101,14 @@ cudaError_t launch_naive(int ops, const double *A, double *B, int64_t n, double 
 
 // K3: the two edge strips [0,T) and [n-T,n) of a slab after its ghosts arrived.
 cudaError_t launch_edges(int ops, const double *A, double *B, int64_t n, int T, double q, double scale,
-                         Guard guard, cudaStream_t st);
+                         Guard guard, const FastRange &fr, cudaStream_t st);
 
 // K3p: K3 fused with a peer-memory halo put (kernels.cu).  my_flags: this slab's two
 // exchange-index words (side 0 at +0, side 1 at +32); put_left/right: where the new
 // left/right strips go in the neighbours' B (their right/left pads); flag_left/right:
 // the neighbours' words for those pads.  Waits for index g, releases g+1.
 cudaError_t launch_edges_put(int ops, const double *A, double *B, int64_t n, int T, double q, double scale,
-                             Guard guard, const unsigned *my_flags, unsigned g, double *put_left, double *put_right,
+                             Guard guard, const FastRange &fr, const unsigned *my_flags, unsigned g, double *put_left, double *put_right,
                              unsigned *flag_left, unsigned *flag_right, cudaStream_t st);
 // Push A[0,T) / A[n-T,n) into the neighbours' pads and release their flags with g+1.
 cudaError_t launch_push_edges(const double *A, int64_t n, int T, unsigned g, double *put_left, double *put_right,
@@ -138,7 +149,8 @@ bool resident_fits(int ops, int64_t n, int T, int num_sms, bool mbox = false);  
 size_t resident_scratch_bytes(int T, int num_sms);
 cudaError_t resident_scratch_init(void *scratch, int T, int num_sms, cudaStream_t st);
 cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
-                            double r, Guard guard, void *scratch, int num_sms, cudaStream_t st, int *warps_out,
+                            double r, Guard guard, const FastRange &fr, void *scratch, int num_sms, cudaStream_t st,
+                            int *warps_out,
                             const MboxArgs &mb = MboxArgs{});
 
 }  // namespace heat1d

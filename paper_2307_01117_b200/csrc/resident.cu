@@ -102,12 +102,13 @@ __device__ __forceinline__ void steps_regs(double (&u)[V], double (&v)[V], int T
 // The guard's fallback (rare): a period with the literal 5-op sequence on the span's
 // row (which holds the period's input), out of line so that its registers do not add
 // to the hot path's.
-template <int V>
+// (OPS = 3: fast mode's fallback when the scaled state could overflow, FastRange)
+template <int V, int OPS = 5>
 __device__ __noinline__ void period_literal(double *row, int Tp, double r, int lane) {
     double u[V], v[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) u[j] = row[lane * V + j];
-    steps_regs<V, 5>(u, v, Tp, r, 1.0);
+    steps_regs<V, OPS>(u, v, Tp, r, 1.0);
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < V; ++j) row[lane * V + j] = u[j];
@@ -119,7 +120,16 @@ __device__ __noinline__ void period_literal(double *row, int Tp, double r, int l
 // The row holds the same cells as u on entry.
 template <int V, int OPS>
 __device__ __forceinline__ void period_steps(double (&u)[V], double (&v)[V], double *row, int Tp, double r,
-                                             double scale, Guard guard, int live, int lane) {
+                                             double scale, Guard guard, int live, int lane, bool scaled,
+                                             double r3) {
+    if constexpr (ops_scaled(OPS)) {
+        if (!scaled) {  // the scaled state could overflow: the contracted 3-op form (coefficient r3)
+            period_literal<V, 3>(row, Tp, r3, lane);
+#pragma unroll
+            for (int j = 0; j < V; ++j) u[j] = row[lane * V + j];
+            return;
+        }
+    }
     if constexpr (ops_guarded(OPS)) {
         GuardAcc acc;
 #pragma unroll
@@ -385,10 +395,10 @@ __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, double
 // MB: the cross-rank mailbox code is compiled in (only then: it costs ~30 registers).
 // DF: data-as-flag halos (V >= 33 spans).
 template <int V, int OPS, bool MB, bool DF>
-__global__ void __launch_bounds__(256, (DF && OPS >= 3 && V <= 33) ? 2 : 0)
+__global__ void __launch_bounds__(256, (DF && V <= 33 && !(MB && OPS == 1)) ? 2 : 0)
 k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t nt, double r,
             double rr, double *__restrict__ edges, unsigned *__restrict__ flags, int Wt, Guard guard,
-            MboxArgs mb_in) {
+            FastRange fr, MboxArgs mb_in) {
     const MboxArgs mb = MB ? mb_in : MboxArgs{};
     extern __shared__ __align__(16) double srow[];
     const int lane = threadIdx.x & 31;
@@ -399,6 +409,7 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
     double *rows = srow + (size_t)wib * (32 * V + 1);
     const Span a = make_span(gw, Ns, n, rows);
     const int live = a.own + 2 * T;
+    const bool scaled = !ops_scaled(OPS) || __shfl_sync(0xffffffffu, (int)scaled_in_range(fr), 0) != 0;
     double ua[V], v[V];
     // scaled variants: r is their coefficient c, rr the true r; r^T per full period
     const double scaleT = ops_scaled(OPS) ? scale_of(rr, T) : 1.0;
@@ -414,7 +425,7 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
     for (unsigned p = 0;; ++p) {
         const int Tp = (int)((nt - done) < T ? (nt - done) : T);
         const double sc = (ops_scaled(OPS) && Tp != T) ? scale_of(rr, Tp) : scaleT;
-        period_steps<V, OPS>(ua, v, a.row, Tp, r, sc, guard, live, lane);
+        period_steps<V, OPS>(ua, v, a.row, Tp, r, sc, guard, live, lane, scaled, fr.r);
         regs_to_row<V>(ua, a.row, lane);
         done += Tp;
         if (done >= nt) break;
@@ -570,8 +581,8 @@ cudaError_t launch_mbox_init(double *mbox, cudaStream_t st) {  // every data slo
 }
 
 cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
-                            double r, Guard guard, void *scratch, int num_sms, cudaStream_t st, int *warps_out,
-                            const MboxArgs &mb) {
+                            double r, Guard guard, const FastRange &fr, void *scratch, int num_sms, cudaStream_t st,
+                            int *warps_out, const MboxArgs &mb) {
     ResPlan p;
     if (!res_plan(ops, n, T, num_sms, &p, mb.on != 0)) return cudaErrorInvalidValue;
     const int64_t ns = p.wt;
@@ -583,7 +594,7 @@ cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int 
     // (data-as-flag: the edge slots are EMPTY already -- resident_scratch_init at create, and
     // every completed launch leaves them so)
     void *args[] = {(void *)&A, (void *)&B, (void *)&n, (void *)&T, (void *)&nt, (void *)&q, (void *)&r,
-                    (void *)&edges, (void *)&flags, (void *)&Wt, (void *)&guard, (void *)&mb};
+                    (void *)&edges, (void *)&flags, (void *)&Wt, (void *)&guard, (void *)&fr, (void *)&mb};
     if (warps_out) *warps_out = Wt;
     return cudaLaunchCooperativeKernel(res_fn(ops, p.rv, mb.on != 0), dim3((unsigned)p.grid),
                                        dim3((unsigned)(p.nw * 32)), args, p.smem, st);

@@ -99,6 +99,9 @@ struct GuardAcc {
     __device__ __forceinline__ bool ok(Guard g) const { return mn >= g.kmin1 && mx <= g.kmax; }
 };
 
+// FastRange (kernels.h): may the scaled fast form run?  (K5 wrote the word in an earlier launch.)
+__device__ __forceinline__ bool scaled_in_range(const FastRange &f) { return !f.absmax || *f.absmax <= f.limit; }
+
 // Cross-rank waits (peer-memory flags) must not hang a process forever if a neighbour
 // rank died or diverged: after HEAT1D_WAIT_NS of polling the kernel traps (the CUDA
 // error poisons the handle; the caller sees HEAT1D_ECUDA instead of a hang).

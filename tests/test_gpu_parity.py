@@ -376,22 +376,24 @@ def test_fast_mode_r_half_is_exact_average(h1):
 
 
 def test_fast_mode_range_fallback(h1):
-    """Values near the top of the fp64 range would overflow the scaled state (|u0| r^-T):
-    set_initial's K5 check falls back to the 3-op form, per initial state."""
+    """Values near the top of the fp64 range would overflow the scaled state (|u0| r^-T): the
+    scaled kernels read K5's max|u0| word on the device and run the 3-op form instead, per
+    initial state -- K2 (+ K3/K3p edge strips with several slabs) and K6."""
     N, nt = 50_000, 40
     u0 = synth.uniform(6, 0, N, -1.0, 1.0)
     big = u0 * 1e300
-    with h1.Heat1D(N, 1, nt, 0.25, 1.0, 1.0, T=32, mode="fast", resident=False) as h:
-        h.set_initial(big)
-        assert h.info()["dp_ops"] == 3
-        h.run(nt)
-        got = h.get()
-        assert np.all(np.isfinite(got))
-        assert np.max(np.abs(got - oracle.run(big, 0.25, nt))) <= fast_bound(big, nt)
-        h.set_initial(u0)                       # back in range: the scaled variant again
-        assert h.info()["dp_ops"] == 2
-        h.run(nt)
-        assert np.max(np.abs(h.get() - oracle.run(u0, 0.25, nt))) <= fast_bound(u0, nt)
+    for kw in (dict(resident=False), dict(resident=True), dict(resident=False, virtual_slabs=2),
+               dict(resident=False, virtual_slabs=2, transport="nccl")):
+        with h1.Heat1D(N, 1, nt, 0.25, 1.0, 1.0, T=32, mode="fast", **kw) as h:
+            assert h.info()["dp_ops"] == 2
+            h.set_initial(big)
+            h.run(nt)
+            got = h.get()
+            assert np.all(np.isfinite(got)), kw
+            assert np.max(np.abs(got - oracle.run(big, 0.25, nt))) <= fast_bound(big, nt), kw
+            h.set_initial(u0)                       # back in range: the scaled variant again
+            h.run(nt)
+            assert np.max(np.abs(h.get() - oracle.run(u0, 0.25, nt))) <= fast_bound(u0, nt), kw
 
 
 def test_fast_mode_c4_first_100_steps(h1):
