@@ -893,3 +893,31 @@ def test_non_blocking_handle_is_stream_ordered(h1, resident):
         assert_bitwise(host_out.numpy(), want, "non-blocking, pinned host buffers")
         assert_bitwise(h.solve_host(u0, nt), want, "non-blocking handle, solve_host returns filled")
     torch.cuda.set_stream(torch.cuda.default_stream())
+
+
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_trace_shows_halo_work_beside_the_interior(h1, transport):
+    """heat1d_trace (profiling): per pass one comm-stream interval (exchange + edge strips)
+    and one compute-stream K2 interval per slab; the comm work of a pass starts before that
+    pass's interior ends (the two streams overlap), and the result is still bitwise."""
+    N, G, T, nt = 4 * 200_000, 4, 16, 16 * 5
+    u0 = synth.uniform(81, 0, N, -1.0, 1.0)
+    with h1.Heat1D(200_000, 4, nt, 0.5, 1.0, 1.0, T=T, virtual_slabs=G, transport=transport,
+                   resident=False) as h:
+        h.set_initial(u0)
+        h.set_profiling(True)
+        h.run(nt)
+        tr = h.trace()
+        n, ms = h.profile()
+        h.set_profiling(False)
+        got = h.get()
+    assert_bitwise(got, oracle.run(u0, 0.5, nt), "traced run")
+    halo = [e for e in tr if e[1] == "halo"]
+    k2 = [e for e in tr if e[1] == "K2"]
+    assert len(halo) == nt // T and len(k2) == G * (nt // T)
+    assert all(e[0] == 1 for e in halo) and all(e[0] == 0 for e in k2)
+    assert n == len(k2) and ms > 0
+    for i, hv in enumerate(halo):
+        ks = k2[i * G:(i + 1) * G]
+        assert all(e[3] >= e[2] >= 0 for e in ks) and hv[3] >= hv[2] >= 0
+        assert hv[2] < max(e[3] for e in ks)   # the halo work starts while the interior runs
