@@ -88,6 +88,9 @@ struct heat1d_s {
     unsigned long long *win_absmax = nullptr;
     int64_t win_absmax_n = 0;
     int64_t stream_windows = 0;  // windows of the last heat1d_solve_host (0 = plain sequence)
+    // test hooks, resolved once at create (fault injection of the tests)
+    unsigned comm_delay_us = 0;  // HEAT1D_COMM_DELAY_US: hold the comm stream before each exchange
+    bool poison_pads = false;    // HEAT1D_POISON_PADS=1: NaN ghost pads at every initial state
     int64_t window_cells = 0;    // > 0: streaming handle (opts.window_cells): only solve_host
     int64_t buf_len = 0;         // doubles per ping-pong buffer of slab 0 (as allocated)
     // transport P2P (several slabs): exchange-index words of this handle's slabs, the
@@ -465,8 +468,8 @@ int run_passes(heat1d_t h, int64_t nt) {
             heat1d_s::ProfRec crec;
             int prc = prof_begin(h, h->comm, &crec, 1, HEAT1D_TRACE_HALO);
             if (prc) return prc;
-            if (const char *dl = getenv("HEAT1D_COMM_DELAY_US")) {  // fault injection (tests)
-                CK(heat1d::launch_delay((unsigned)atoi(dl), h->comm));
+            if (h->comm_delay_us) {  // fault injection (tests)
+                CK(heat1d::launch_delay(h->comm_delay_us, h->comm));
                 h->launches++;
             }
             int rc = HEAT1D_OK;
@@ -1135,6 +1138,8 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
         }
         h->mbox_left = h->mbox_right = h->mbox;
     }
+    if (const char *dl = getenv("HEAT1D_COMM_DELAY_US")) h->comm_delay_us = (unsigned)atoi(dl);
+    if (const char *pp = getenv("HEAT1D_POISON_PADS")) h->poison_pads = atoi(pp) == 1;
     // HEAT1D_GEOM (tuning knob) only where the pass kernel exists for every arithmetic variant
     // this handle may run (its matched/fast form and the 3-op fallback); else the default
     if (!parse_geom_env(&h->geom) || !heat1d::pass_supported(h->geom, h->ops) ||
@@ -1184,7 +1189,7 @@ static int check_fast_range(heat1d_t h) {
 }
 
 static int after_initial(heat1d_t h) {
-    if (h->multi() && h->nranks == 1 && getenv("HEAT1D_POISON_PADS") && atoi(getenv("HEAT1D_POISON_PADS")) == 1) {
+    if (h->multi() && h->nranks == 1 && h->poison_pads) {
         // fault injection (tests): NaN in every ghost pad of both buffers -- any pad value
         // read before the exchange refreshed it would poison the result
         for (const Slab &s : h->slabs)
