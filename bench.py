@@ -570,6 +570,8 @@ def main():
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "GLUPS", "cores": 1, "kind": "oracle", "sample": "failed: %s" % e}
 
+    if world > 1:
+        dist.barrier()  # every rank is quiet (no NCCL logging) while rank 0 prints its line
     if rank == 0:
         ms = main_m["ms"]
         nslab = world * args.virtual_slabs
@@ -597,6 +599,7 @@ def main():
         }
         emit(line, args)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 
