@@ -325,9 +325,13 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
             int64_t x0, x1, ld_lo, ld_hi;
             span_of(tile, &x0, &x1, &ld_lo, &ld_hi);
             const uint32_t bytes = (uint32_t)((ld_hi - ld_lo) * 8);
+            HCHECK(bytes <= stage_doubles * 8u);                     // the stage holds the tile input
+            HCHECK(ld_lo >= -(int64_t)T - 1 && ld_hi <= n + T + 1);  // within the padded slab
+            HCHECK((128 + (size_t)S * stage_doubles * 8 + (size_t)2 * NW * 2 * KX * 8) <= dynamic_smem_bytes());
             mbar_arrive_expect_tx(&full[s], bytes);
             bulk_g2s(stages + (size_t)s * stage_doubles, A + ld_lo, bytes, &full[s], pol_in);
         };
+        HCHECK(out_lo >= 0 && out_hi <= n && wrapT <= n && wrapT <= 128);  // (wrapT: the pad fill, <= T_MAX)
         if (lane == 0) {
             for (int i = 0; i < S; ++i) {
                 const int64_t tile = blockIdx.x + i * stride;
@@ -389,6 +393,7 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
         const int sh = (int)((x0 - T) & 1);
         mbar_wait_sleep(&full[s], par);
         const int base = sh + warp * SW + lane * V;
+        HCHECK(base >= 0 && base + V <= (int)stage_doubles);
         double u[V];
 #pragma unroll
         for (int j = 0; j < V; ++j) u[j] = st[base + j];
@@ -588,6 +593,7 @@ __global__ void __launch_bounds__(96) k3_edges(const double *__restrict__ A, dou
     __shared__ double w[2][3 * 128];
     const int64_t base = (blockIdx.x == 0) ? -(int64_t)T : n - 2 * (int64_t)T;
     const int len = 3 * T;
+    HCHECK(T >= 1 && T <= 128 && n >= (int64_t)T);  // windows [-T, 2T), [n-2T, n+T) inside the pads
     for (int i = threadIdx.x; i < len; i += blockDim.x) w[0][i] = A[base + i];
     __syncthreads();
     bool scaled;
@@ -648,6 +654,7 @@ __global__ void __launch_bounds__(96) k3_edges_put(const double *__restrict__ A,
     __syncthreads();
     const int64_t base = (side == 0) ? -(int64_t)T : n - 2 * (int64_t)T;
     const int len = 3 * T;
+    HCHECK(T >= 1 && T <= 128 && n >= 2 * (int64_t)T);
     for (int i = threadIdx.x; i < len; i += blockDim.x) w[0][i] = __ldcv(A + base + i);  // pads: peer-written
     __syncthreads();
     bool scaled;

@@ -409,6 +409,9 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
     double *rows = srow + (size_t)wib * (32 * V + 1);
     const Span a = make_span(gw, Ns, n, rows);
     const int live = a.own + 2 * T;
+    HCHECK(live <= 32 * V && a.own >= T && a.start + a.own <= n);  // the span and its halos fit
+    HCHECK((size_t)(blockDim.x >> 5) * (32 * V + 1) * 8 <= dynamic_smem_bytes());
+    HCHECK(T <= MBOX_TMAX);
     const bool scaled = !ops_scaled(OPS) || __shfl_sync(0xffffffffu, (int)scaled_in_range(fr), 0) != 0;
     double ua[V], v[V];
     // scaled variants: r is their coefficient c, rr the true r; r^T per full period

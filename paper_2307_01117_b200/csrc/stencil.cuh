@@ -102,6 +102,31 @@ struct GuardAcc {
 // FastRange (kernels.h): may the scaled fast form run?  (K5 wrote the word in an earlier launch.)
 __device__ __forceinline__ bool scaled_in_range(const FastRange &f) { return !f.absmax || *f.absmax <= f.limit; }
 
+// Bounds checks of a checked measurement build (tools/ab_build.py checked=HEAT1D_CHECKED; the
+// pool's compute-sanitizer is closed): every shared/global index the kernels derive is
+// asserted; a violation prints and traps (the handle reports ECUDA).  No code otherwise.
+#ifdef HEAT1D_CHECKED
+#include <cstdio>
+#define HCHECK(cond)                                                                          \
+    do {                                                                                      \
+        if (!(cond)) {                                                                        \
+            printf("HCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                        \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define HCHECK(cond) \
+    do {             \
+    } while (0)
+#endif
+
+__device__ __forceinline__ uint32_t dynamic_smem_bytes() {
+    uint32_t b;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(b));
+    return b;
+}
+
 // Cross-rank waits (peer-memory flags) must not hang a process forever if a neighbour
 // rank died or diverged: after HEAT1D_WAIT_NS of polling the kernel traps (the CUDA
 // error poisons the handle; the caller sees HEAT1D_ECUDA instead of a hang).
