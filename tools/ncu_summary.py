@@ -4,6 +4,7 @@
     python tools/ncu_summary.py report gpurun_out/k2p_c4.ncu-rep  > profiles/r01_ncu_k2p_c4.txt
     python tools/ncu_summary.py launches gpurun_out/launches_c4.csv > profiles/r01_launches_c4.txt
     python tools/ncu_summary.py traffic gpurun_out/k2p_c4.ncu-rep KEY profiles/ncu_traffic.json
+    python tools/ncu_summary.py stalls gpurun_out/k2p_c4.ncu-rep   > profiles/r02_ncu_..._stalls.txt
 """
 import collections
 import csv
@@ -69,6 +70,51 @@ def traffic(path, key, out_json):
     print(key, t)
 
 
+def stalls(path):
+    """Warp-state samples of a --set full capture: totals per reason, per opcode, hottest SASS."""
+    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hi = [i for i, r in enumerate(rows) if "Address" in r and "Source" in r][0]
+    hdr, data = rows[hi], rows[hi + 1:]
+    isrc, iex = hdr.index("Source"), hdr.index("Instructions Executed")
+    reasons = [c for c in hdr if c.startswith("stall_") and "(" not in c]
+    ix = {c: hdr.index(c) for c in reasons}
+
+    def num(r, i):
+        try:
+            return float(r[i] or 0)
+        except (ValueError, IndexError):
+            return 0.0
+
+    def opcode(r):
+        t = r[isrc].split()
+        o = t[1] if t and t[0].startswith("@") and len(t) > 1 else (t[0] if t else "")
+        return o.split(".")[0]
+
+    per_reason = collections.Counter()
+    per_op = collections.defaultdict(collections.Counter)
+    per_ins = []
+    for r in data:
+        c = collections.Counter({k: num(r, ix[k]) for k in reasons})
+        per_reason.update(c)
+        per_op[opcode(r)].update(c)
+        per_ins.append((sum(c.values()), r, c))
+    tot = sum(per_reason.values()) or 1.0
+    print("total samples %d" % tot)
+    for k, v in per_reason.most_common():
+        print("  %-22s %7d %5.1f%%" % (k, v, 100 * v / tot))
+    print("by opcode (top):")
+    for o in sorted(per_op, key=lambda o: -sum(per_op[o].values()))[:14]:
+        c = per_op[o]
+        top = ", ".join("%s %d" % (k[6:], v) for k, v in c.most_common(4) if v)
+        print("  %-8s %8d %5.1f%%   %s" % (o, sum(c.values()), 100 * sum(c.values()) / tot, top))
+    print("top instructions:")
+    for n, r, c in sorted(per_ins, key=lambda t: -t[0])[:12]:
+        top = ", ".join("%s %d" % (k[6:], v) for k, v in c.most_common(3) if v)
+        print("  %s %6d %4.1f%% ex=%s %-50s %s" % (r[0][-4:], n, 100 * n / tot, r[iex], r[isrc][:50], top))
+
+
 def launches(path):
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
@@ -100,3 +146,5 @@ if __name__ == "__main__":
         launches(sys.argv[2])
     elif cmd == "traffic":
         traffic(sys.argv[2], sys.argv[3], sys.argv[4])
+    elif cmd == "stalls":
+        stalls(sys.argv[2])
