@@ -216,8 +216,10 @@ def get_unique_id() -> bytes:
     return buf.raw
 
 
-def _data_ptr(a):
-    """(pointer, nbytes, keepalive) for a numpy array or torch tensor of float64."""
+def _data_ptr(a, out: bool = False):
+    """(pointer, count, keepalive) for a numpy array or torch tensor of float64.  Inputs may
+    be converted (a contiguous float64 copy); an output (`out`) must already be one, since
+    the library writes through the pointer."""
     try:
         import torch
         if isinstance(a, torch.Tensor):
@@ -226,6 +228,10 @@ def _data_ptr(a):
             return a.data_ptr(), a.numel(), a
     except ImportError:
         pass
+    if out:
+        if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous and a.flags.writeable):
+            raise TypeError("out must be a writeable C-contiguous float64 array or tensor")
+        return a.ctypes.data, a.size, a
     arr = np.ascontiguousarray(a, dtype=np.float64)
     return arr.ctypes.data, arr.size, arr
 
@@ -262,7 +268,10 @@ class Heat1D:
         o.window_cells = window_cells
         self._dev_buf = dev_buf  # caller-owned state memory (torch tensor): kept alive with the handle
         if dev_buf is not None:
-            ptr, n, _ = _data_ptr(dev_buf)
+            import torch
+            if not (isinstance(dev_buf, torch.Tensor) and dev_buf.is_cuda):
+                raise TypeError("dev_buf must be a CUDA tensor (device memory the handle computes in)")
+            ptr, n, _ = _data_ptr(dev_buf, out=True)
             need = buffer_len(nx, np_, o)
             if n < need:
                 raise ValueError("dev_buf holds %d doubles, the handle needs %d (buffer_len)" % (n, need))
@@ -332,7 +341,7 @@ class Heat1D:
     def get(self, out=None):
         if out is None:
             out = np.empty(self.count, dtype=np.float64)
-        ptr, n, keep = _data_ptr(out)
+        ptr, n, keep = _data_ptr(out, out=True)
         _check(self._lib.heat1d_get(self._h, ctypes.c_void_p(ptr), n), self._h)
         return out
 
@@ -342,7 +351,7 @@ class Heat1D:
         if out is None:
             out = np.empty(self.count, dtype=np.float64)
         pi, n, keep_in = _data_ptr(u0)
-        po, m, keep_out = _data_ptr(out)
+        po, m, keep_out = _data_ptr(out, out=True)
         if n != self.count or m != self.count:
             raise ValueError("u0 and out must hold the local slab (%d cells)" % self.count)
         _check(self._lib.heat1d_solve_host(self._h, ctypes.c_void_p(pi), n, -1 if nt is None else nt,
@@ -357,7 +366,7 @@ class Heat1D:
         pi, n, k1 = _data_ptr(u0)
         pl, nl, k2 = _data_ptr(left)
         pr, nr, k3 = _data_ptr(right)
-        po, m, k4 = _data_ptr(out)
+        po, m, k4 = _data_ptr(out, out=True)
         steps = -1 if nt is None else nt
         if n != self.count or m != self.count or (nt is not None and (nl < nt or nr < nt)):
             raise ValueError("u0/out must hold the slab and left/right at least nt cells")

@@ -162,3 +162,22 @@ def test_exchange_plan(lib):
     assert (p.left, p.right) == (0, 0)
     with pytest.raises(h1.Heat1DError):
         h1.plan_exchange(4, 2, 2, 0, 5)              # halo deeper than a slab
+
+
+def test_binding_output_buffers_are_never_copies():
+    """The binding converts inputs (a contiguous float64 copy is fine to read from) but refuses an
+    output it would have to copy: the library writes through the pointer, so a converted `out`
+    would silently lose the result."""
+    import numpy as np
+    from paper_2307_01117_b200 import heat1d as hb
+    ptr, n, keep = hb._data_ptr([1, 2, 3])                      # input: converted
+    assert n == 3 and keep.dtype == np.float64
+    good = np.zeros(8)
+    assert hb._data_ptr(good, out=True)[0] == good.ctypes.data  # output: used in place
+    for bad in (np.zeros(8, dtype=np.float32), np.zeros(16)[::2], np.zeros((2, 4)).T, [0.0] * 8):
+        with pytest.raises(TypeError):
+            hb._data_ptr(bad, out=True)
+    ro = np.zeros(8)
+    ro.flags.writeable = False
+    with pytest.raises(TypeError):
+        hb._data_ptr(ro, out=True)
