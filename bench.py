@@ -599,8 +599,12 @@ def main():
         }
         emit(line, args)
     if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+        # the JSON line is the last thing on stdout: tearing down the process group (or letting
+        # interpreter exit do it) would print NCCL's INIT-subsystem "Destroy/Abort COMPLETE"
+        # lines after it; every GPU stream is idle and every library handle is closed by now
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
 
 
 if __name__ == "__main__":
