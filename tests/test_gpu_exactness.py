@@ -180,3 +180,20 @@ def test_mailbox_loopback_extremes(h1, monkeypatch):
                 h.run(nt)
                 want = oracle.run(want, 0.5, nt)
                 assert_same(h.get(), want, "mailbox %s" % recipe)
+
+
+@pytest.mark.parametrize("recipe", ["subnormal", "straddle", "top1022", "huge1023", "below1022"])
+@pytest.mark.parametrize("k,ops", [(0.75, 4), (2.0, 3)])
+@pytest.mark.parametrize("resident", [False, True])
+def test_unstable_r_extremes(h1, recipe, k, ops, resident):
+    """r > 1/2 (allow_unstable): the guard's top bound takes the growth factor G = 4r per step
+    (DESIGN.md c3), and r = 2 (a power of two >= 1) runs the 3-op form with no bottom bound (2*t is
+    exact down to the subnormals).  The state grows like |1 - 4r|^t, so huge rings overflow to
+    inf / NaN within a few steps -- compared NaN-aware, bitwise elsewhere."""
+    N, T = 50_003, 8
+    nt = 2 * T + 3
+    u0 = RECIPES[recipe](N)
+    want = oracle.run(u0, k, nt)
+    got, info = run_gpu(h1, u0, nt, k, T=T, resident=resident, allow_unstable=True)
+    assert info["dp_ops"] == ops and info["resident"] == (1 if resident else 0)
+    assert_same(got, want, "r=%g %s resident=%s" % (k, recipe, resident))

@@ -56,6 +56,26 @@ def step_fma3(u: np.ndarray, r: float) -> np.ndarray:
     return out
 
 
+def step_fma4(u: np.ndarray, r: float) -> np.ndarray:
+    """One Jacobi step of the 4-op matched form (any r): fma(-2,b,a), + c, r *, b + (the GPU's
+    OPS_MATCHED4)."""
+    n = u.size
+    out = np.empty_like(u)
+    for i in range(n):
+        a, b, c = float(u[(i - 1) % n]), float(u[i]), float(u[(i + 1) % n])
+        t = fma(-2.0, b, a) + c
+        out[i] = b + r * t
+    return out
+
+
+def top_passes(u: np.ndarray, r: float, Tp: int) -> bool:
+    """The guard's top bound (kernels.h guard_of): |x| < 2^(E-1023), E = 2045 - ceil(Tp log2 G),
+    G = 1 for r <= 1/2, 4r above."""
+    G = 4.0 * r if r > 0.5 else 1.0
+    E = 2045 - math.ceil(Tp * math.log2(G))
+    return bool(np.all(np.abs(u) < math.ldexp(1.0, E - 1023)))
+
+
 def guard_passes(u: np.ndarray, r: float, Tp: int) -> bool:
     """The guard of stencil.cuh for the 3-op form and r = 2^-j <= 1/2, restated from the theory."""
     j = -int(round(math.log2(r)))
@@ -160,3 +180,32 @@ def test_top_bound_blocks_equal_the_literal_sequence():
             lit = oracle.run(lit, r, 1)
             f3 = step_fma3(f3, r)
         assert np.array_equal(lit.view(np.uint64), f3.view(np.uint64))
+
+
+@pytest.mark.parametrize("r,Tp", [(0.75, 4), (0.6, 6), (0.4, 5), (3.0, 2)])
+def test_top_bound_4op_including_unstable_r(r, Tp):
+    """4-op form near the top of the range, r > 1/2 included (the G = 4r branch): blocks whose cells
+    pass the top bound equal the literal sequence after every step; rings of values just below the
+    bound and just above it (some above fail it, and there 2b overflows in the oracle)."""
+    G = 4.0 * r if r > 0.5 else 1.0
+    e_top = 2045 - math.ceil(Tp * math.log2(G)) - 1023     # |x| < 2^e_top passes
+    passed = failed = 0
+    for seed in range(30):
+        # ring() values with exponent e are < 2^(e+1): e <= e_top - 1 passes; every third ring
+        # also draws exponents above the bound
+        hi = e_top - 1 if seed % 3 else min(e_top + 2, 1022)
+        u0 = ring(9000 + 31 * Tp + seed, 18, e_top - 6, hi)
+        if not top_passes(u0, r, Tp):
+            failed += 1
+            continue
+        passed += 1
+        lit, f4 = u0.copy(), u0.copy()
+        for s in range(Tp):
+            lit = oracle.run(lit, r, 1)
+            f4 = step_fma4(f4, r)
+            assert np.array_equal(lit.view(np.uint64), f4.view(np.uint64)), (seed, s)
+    assert passed >= 5 and failed >= 1
+    # a cell at 2^1023 (above every bound): the oracle's 2.0*b overflows, fma(-2, b, a) does not
+    big = np.array([1.75 * 2.0 ** 1023, 2.0 ** 1023, 1.0])
+    assert not top_passes(big, r, Tp)
+    assert np.isinf(oracle.run(big, r, 1)[1]) and np.isfinite(step_fma4(big, r)[1])
