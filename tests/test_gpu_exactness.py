@@ -197,3 +197,20 @@ def test_unstable_r_extremes(h1, recipe, k, ops, resident):
     got, info = run_gpu(h1, u0, nt, k, T=T, resident=resident, allow_unstable=True)
     assert info["dp_ops"] == ops and info["resident"] == (1 if resident else 0)
     assert_same(got, want, "r=%g %s resident=%s" % (k, recipe, resident))
+
+
+@pytest.mark.parametrize("resident", [False, True])
+def test_nonfinite_inputs(h1, resident):
+    """u0 holding +-inf and NaN cells (special values are states too): the guard rejects their
+    blocks (exponent 0x7ff is above every top bound), so those blocks run the literal sequence and
+    the inf/NaN fronts spread exactly as in the oracle; everything else stays bitwise."""
+    N, T = 60_001, 16
+    nt = 3 * T + 1
+    u0 = synth.uniform(21, 0, N, -1.0, 1.0)
+    u0[[5, 20_000]] = np.inf
+    u0[[7_777, 40_000]] = -np.inf
+    u0[[33_333, N - 1]] = np.nan
+    want = oracle.run(u0, 0.5, nt)
+    got, _ = run_gpu(h1, u0, nt, 0.5, T=T, resident=resident)
+    assert_same(got, want, "non-finite u0 resident=%s" % resident)
+    assert np.isnan(want).sum() > 0 and np.isfinite(want).sum() > N // 2
