@@ -77,6 +77,7 @@ struct heat1d_s {
     double *mbox = nullptr, *mbox_left = nullptr, *mbox_right = nullptr;
     bool mbox_ipc_left = false, mbox_ipc_right = false;
     unsigned k6_base = 0;  // global exchange index of the next K6 launch
+    unsigned k6_tag = 1;   // edge tag of the next K6 launch's first period (resident.cu tagged words)
     void *res_scratch = nullptr;
     int res_warps = 0;
 
@@ -418,9 +419,18 @@ int run_resident(heat1d_t h, int64_t nt) {
         // still read it (resident.cu, mbox_publish)
         h->k6_base += (unsigned)((nt + h->T - 1) / h->T) + 2u;
     }
+    // edge tags: unique per launch and period; before the 32-bit counter would wrap, the slots
+    // go back to tag 0 and the count restarts (a stale tag must never equal a live one)
+    const unsigned periods = (unsigned)((nt + h->T - 1) / h->T);
+    if (h->k6_tag > 0xffffffffu - periods - 4u) {
+        CK(heat1d::resident_scratch_init(h->res_scratch, h->T, h->num_sms, h->stream));
+        h->k6_tag = 1;
+    }
+    const unsigned tbase = h->k6_tag;
+    h->k6_tag += periods + 2u;
     CK(heat1d::launch_resident(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, h->T, nt, h->q,
                                h->r, guard_for(h, h->ops, h->T), fast_range(h, h->ops, h->absmax), h->res_scratch,
-                               h->num_sms, h->stream, &h->res_warps, mb));
+                               h->num_sms, h->stream, &h->res_warps, mb, tbase));
     h->launches++;
     rc = prof_end(h, h->stream, rec);
     if (rc) return rc;

@@ -150,7 +150,7 @@ size_t resident_scratch_bytes(int T, int num_sms);
 cudaError_t resident_scratch_init(void *scratch, int T, int num_sms, cudaStream_t st);
 cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
                             double r, Guard guard, const FastRange &fr, void *scratch, int num_sms, cudaStream_t st,
-                            int *warps_out,
-                            const MboxArgs &mb = MboxArgs{});
+                            int *warps_out, const MboxArgs &mb,
+                            unsigned tbase);  // tag of this launch's first period (>= 1, new per launch)
 
 }  // namespace heat1d

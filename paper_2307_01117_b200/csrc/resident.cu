@@ -11,10 +11,10 @@
 //
 // Synchronisation is pairwise, no grid-wide barrier: spans of V = 17 cells per
 // lane (periods T <= 32) publish their edges with a release of a per-span flag;
-// spans of V >= 33 (the default period T = 64) use data-as-flag slots (below).
-// Edge buffers are double-buffered by period parity: a span writes period p+2
-// edges only after its neighbours published p+1, i.e. after they finished
-// reading period p.
+// spans of V >= 33 (the default period T = 64) publish tagged words (below): no
+// flag, no fence.  Edge buffers are double-buffered by period parity: a span
+// writes period p+2 edges only after its neighbours published p+1, i.e. after
+// they finished reading period p.
 //
 // Guarded variants (OPS 4, 3; stencil.cuh): at the start of every period a warp
 // checks the cells of its span (owned + halos) and, if any fails, advances that
@@ -234,19 +234,46 @@ __device__ __forceinline__ void fence_acq_rel() {
 // arithmetic on either NaN gives the same canonical NaN)
 constexpr unsigned long long HEAT1D_EMPTY_QUIET = HEAT1D_EMPTY | (1ull << 51);
 
+// Tagged words (the spans' edges inside one GPU, V >= 33): an edge value travels as two
+// 8-byte words (tag << 32) | half, stored by one st.v2.b64.  Each naturally aligned 8-byte
+// element of a vector access is single-copy atomic (PTX memory model), so a reader that
+// finds the expected tag in both words holds both halves of that one write.  Tags are
+// unique per launch and period (tbase + p, the host advances tbase past every launch), so a
+// slot's stale content never matches; the reader writes nothing back and nobody fences:
+// a span overwrites a slot (period p+2) only after computing from its neighbour's period
+// p+1 edges, which that neighbour computed from the period-p values it read (a data
+// dependency orders its read before its next publish).
+__device__ __forceinline__ void st_tagged(unsigned long long *p, double v, unsigned tag) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const unsigned long long t = (unsigned long long)tag << 32;
+    asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(t | (b & 0xffffffffull)),
+                 "l"(t | (b >> 32))
+                 : "memory");
+}
+__device__ __forceinline__ bool ld_tagged(const unsigned long long *p, unsigned tag, double *v) {
+    unsigned long long w0, w1;
+    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+    *v = __longlong_as_double((long long)((w1 << 32) | (w0 & 0xffffffffull)));
+    return (unsigned)(w0 >> 32) == tag && (unsigned)(w1 >> 32) == tag;
+}
+// the tagged edge slots of span `id`, period parity `par`, side `side` (2 words per cell)
+__device__ __forceinline__ unsigned long long *tagged_slot(double *edges, int id, unsigned par, int side, int T) {
+    return reinterpret_cast<unsigned long long *>(edges) + (((size_t)id * 4 + par * 2 + side) * T) * 2;
+}
+
 // edges: [Ns][2 parities][2 sides][T]; publish this span's period-p edges
 // (DF: data-as-flag protocol, compiled into its own kernel instantiation)
-template <bool DF = false, bool SYS = false>
+template <bool DF = false>
 __device__ __forceinline__ void publish(const Span &s, int T, unsigned p, double *edges, unsigned *flags,
-                                        int lane) {
-    double *E = edges + ((size_t)s.id * 4 + (p & 1) * 2) * T;
+                                        unsigned tbase, int lane) {
     if constexpr (DF) {
-        fence_acq_rel<SYS>();  // earlier slot resets (local and, SYS, in the mailbox) before this data
+        unsigned long long *E0 = tagged_slot(edges, s.id, p & 1, 0, T), *E1 = tagged_slot(edges, s.id, p & 1, 1, T);
         for (int i = lane; i < T; i += 32) {
-            st_relaxed_u64<SYS>(E + i, s.row[T + i]);
-            st_relaxed_u64<SYS>(E + T + i, s.row[s.own + i]);
+            st_tagged(E0 + 2 * i, s.row[T + i], tbase + p);
+            st_tagged(E1 + 2 * i, s.row[s.own + i], tbase + p);
         }
     } else {
+        double *E = edges + ((size_t)s.id * 4 + (p & 1) * 2) * T;
         for (int i = lane; i < T; i += 32) {
             E[i] = s.row[T + i];          // side 0: first T owned cells
             E[T + i] = s.row[s.own + i];  // side 1: last T owned cells
@@ -273,10 +300,9 @@ __device__ __forceinline__ unsigned *mbox_flag(double *mb, int side) {
 // slot (EMPTY until written, reset by its reader), no flag; the fence orders this rank's
 // earlier resets of its own mailbox before the data that lets the neighbour reuse them.
 template <bool DF = false>
-__device__ __forceinline__ void mbox_publish(const Span &s, int Ns, int T, unsigned g, const MboxArgs &mb, int lane,
-                                             bool fenced = false) {
+__device__ __forceinline__ void mbox_publish(const Span &s, int Ns, int T, unsigned g, const MboxArgs &mb, int lane) {
     if constexpr (DF) {
-        if (!fenced) fence_acq_rel<true>();  // (publish<DF, true> just issued one)
+        fence_acq_rel<true>();
         auto put = [&](double *D, const double *src) {
             for (int i = lane; i < T; i += 32) {
                 double x = src[i];
@@ -307,33 +333,53 @@ __device__ __forceinline__ void mbox_publish(const Span &s, int Ns, int T, unsig
 // on, the slab's outer halos come from the neighbour ranks (exchange index g)
 // initial: the exchange of the initial state (only the remote sides; the local halos
 // were loaded from the slab).
-// Data-as-flag halo refresh, kept out of line: inlined into the period loop its 64-bit
+// Halo refresh of a V >= 33 span, kept out of line: inlined into the period loop its 64-bit
 // polls and pointers raised the matched kernels from 115 to 154 registers (and -25 %).
+// A side is either tagged (a neighbour span on this GPU: L2/R2, expected tag `tag`) or a
+// data-as-flag mailbox slot (a neighbour rank: LE/RE, EMPTY until written, reset by us).
 // doL/doR false: that side's halo is already valid (the initial exchange of local sides).
 template <bool SYS>
-__device__ __noinline__ void refresh_df(double *row, int own, int T, double *LE, double *RE, bool doL, bool doR,
-                                        int lane) {
+__device__ __noinline__ void refresh_df(double *row, int own, int T, const unsigned long long *L2,
+                                        const unsigned long long *R2, double *LE, double *RE, bool doL, bool doR,
+                                        unsigned tag, int lane) {
     const unsigned long long t0 = SYS ? globaltimer_ns() : 0;
     for (int i0 = 0; i0 < T; i0 += 32) {
         const int i = i0 + lane;
-        unsigned long long l = 0, rr = 0;
+        double lv = 0.0, rv = 0.0;
         bool ok;
         do {
+            bool lok = true, rok = true;
             if (i < T) {
-                if (doL) l = ld_relaxed_u64<SYS>(LE + i);
-                if (doR) rr = ld_relaxed_u64<SYS>(RE + i);
+                if (doL) {
+                    if (L2) {
+                        lok = ld_tagged(L2 + 2 * i, tag, &lv);
+                    } else {
+                        const unsigned long long l = ld_relaxed_u64<SYS>(LE + i);
+                        lok = l != HEAT1D_EMPTY;
+                        lv = __longlong_as_double((long long)l);
+                    }
+                }
+                if (doR) {
+                    if (R2) {
+                        rok = ld_tagged(R2 + 2 * i, tag, &rv);
+                    } else {
+                        const unsigned long long rr = ld_relaxed_u64<SYS>(RE + i);
+                        rok = rr != HEAT1D_EMPTY;
+                        rv = __longlong_as_double((long long)rr);
+                    }
+                }
             }
-            ok = i >= T || ((!doL || l != HEAT1D_EMPTY) && (!doR || rr != HEAT1D_EMPTY));
+            ok = lok && rok;
             if (SYS && globaltimer_ns() - t0 > HEAT1D_WAIT_NS) __trap();  // a neighbour rank is gone
         } while (!__all_sync(0xffffffffu, ok));
         if (i < T) {
             if (doL) {
-                row[i] = __longlong_as_double((long long)l);
-                st_relaxed_u64<SYS>(LE + i, __longlong_as_double((long long)HEAT1D_EMPTY));
+                row[i] = lv;
+                if (!L2) st_relaxed_u64<SYS>(LE + i, __longlong_as_double((long long)HEAT1D_EMPTY));
             }
             if (doR) {
-                row[own + T + i] = __longlong_as_double((long long)rr);
-                st_relaxed_u64<SYS>(RE + i, __longlong_as_double((long long)HEAT1D_EMPTY));
+                row[own + T + i] = rv;
+                if (!R2) st_relaxed_u64<SYS>(RE + i, __longlong_as_double((long long)HEAT1D_EMPTY));
             }
         }
     }
@@ -343,12 +389,14 @@ __device__ __noinline__ void refresh_df(double *row, int own, int T, double *LE,
 template <bool DF = false, bool SYS = false>
 __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, double *edges,
                                         const unsigned *flags, int lane, int Ns, const MboxArgs &mb,
-                                        unsigned g, bool initial = false) {
+                                        unsigned g, unsigned tbase, bool initial = false) {
     const bool lrem = mb.on && s.id == 0, rrem = mb.on && s.id == Ns - 1;
     if constexpr (DF) {
-        double *LE = lrem ? mbox_data(mb.self, 0, g) : edges + ((size_t)s.left * 4 + (p & 1) * 2) * T + T;
-        double *RE = rrem ? mbox_data(mb.self, 1, g) : edges + ((size_t)s.right * 4 + (p & 1) * 2) * T;
-        refresh_df<SYS>(s.row, s.own, T, LE, RE, lrem || !initial, rrem || !initial, lane);
+        // left neighbour's side 1 and right neighbour's side 0, or this rank's mailbox
+        refresh_df<SYS>(s.row, s.own, T, lrem ? nullptr : tagged_slot(edges, s.left, p & 1, 1, T),
+                        rrem ? nullptr : tagged_slot(edges, s.right, p & 1, 0, T),
+                        lrem ? mbox_data(mb.self, 0, g) : nullptr, rrem ? mbox_data(mb.self, 1, g) : nullptr,
+                        lrem || !initial, rrem || !initial, tbase + p, lane);
         return;
     }
     if (lrem || rrem) {
@@ -398,7 +446,7 @@ template <int V, int OPS, bool MB, bool DF>
 __global__ void __launch_bounds__(256, (DF && V <= 33 && !(MB && OPS == 1)) ? 2 : 0)
 k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t nt, double r,
             double rr, double *__restrict__ edges, unsigned *__restrict__ flags, int Wt, Guard guard,
-            FastRange fr, MboxArgs mb_in) {
+            FastRange fr, MboxArgs mb_in, unsigned tbase) {
     const MboxArgs mb = MB ? mb_in : MboxArgs{};
     extern __shared__ __align__(16) double srow[];
     const int lane = threadIdx.x & 31;
@@ -421,7 +469,7 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
 
     if (mb.on && (a.id == 0 || a.id == Ns - 1)) {  // outer halos of the initial state: neighbour ranks
         mbox_publish<DF>(a, Ns, T, mb.base, mb, lane);
-        refresh<DF, MB>(a, T, 0, edges, flags, lane, Ns, mb, mb.base, true);
+        refresh<DF, MB>(a, T, 0, edges, flags, lane, Ns, mb, mb.base, tbase, true);
         row_to_regs<V>(a.row, ua, lane);
     }
     int64_t done = 0;
@@ -435,12 +483,12 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
         // system scope only for the slab's two boundary spans (their halos cross GPUs):
         // a .sys fence in every warp every period cost more than half of C5's speed
         if (MB && mb.on && (a.id == 0 || a.id == Ns - 1)) {
-            publish<DF, true>(a, T, p, edges, flags, lane);
-            mbox_publish<DF>(a, Ns, T, mb.base + 1 + p, mb, lane, true);
-            refresh<DF, true>(a, T, p, edges, flags, lane, Ns, mb, mb.base + 1 + p);
+            publish<DF>(a, T, p, edges, flags, tbase, lane);
+            mbox_publish<DF>(a, Ns, T, mb.base + 1 + p, mb, lane);
+            refresh<DF, true>(a, T, p, edges, flags, lane, Ns, mb, mb.base + 1 + p, tbase);
         } else {
-            publish<DF, false>(a, T, p, edges, flags, lane);
-            refresh<DF, false>(a, T, p, edges, flags, lane, Ns, mb, mb.base + 1 + p);
+            publish<DF>(a, T, p, edges, flags, tbase, lane);
+            refresh<DF, false>(a, T, p, edges, flags, lane, Ns, mb, mb.base + 1 + p, tbase);
         }
         row_to_regs<V>(a.row, ua, lane);
     }
@@ -562,17 +610,16 @@ __global__ void k6_fill_empty(double *edges, int64_t count) {
         edges[i] = __longlong_as_double((long long)HEAT1D_EMPTY);
 }
 
+// edges: [Ns][2 parities][2 sides][T] cells, 16 B each (tagged words; the V = 17 flag
+// protocol uses the first half as plain doubles), then the per-span flags
 size_t resident_scratch_bytes(int T, int num_sms) {
     const int64_t ns = (int64_t)num_sms * (MAX_WPS_ANY + MAX_NW);  // >= any plan's wt
-    return (size_t)ns * 4 * T * sizeof(double) + (size_t)ns * sizeof(unsigned) + 256;
+    return (size_t)ns * 4 * T * 16 + (size_t)ns * sizeof(unsigned) + 256;
 }
 
 cudaError_t resident_scratch_init(void *scratch, int T, int num_sms, cudaStream_t st) {
-    // every edge slot of the largest plan EMPTY once per handle: a complete run consumes and
-    // resets every slot it publishes, so the data-as-flag invariant holds from run to run
-    const int64_t ns = (int64_t)num_sms * (MAX_WPS_ANY + MAX_NW);  // >= any plan's wt
-    k6_fill_empty<<<148, 256, 0, st>>>(static_cast<double *>(scratch), ns * 4 * (int64_t)T);
-    return cudaGetLastError();
+    // tag 0 everywhere: launches use tags >= 1 (launch_resident's tbase)
+    return cudaMemsetAsync(scratch, 0, resident_scratch_bytes(T, num_sms), st);
 }
 
 
@@ -585,19 +632,19 @@ cudaError_t launch_mbox_init(double *mbox, cudaStream_t st) {  // every data slo
 
 cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
                             double r, Guard guard, const FastRange &fr, void *scratch, int num_sms, cudaStream_t st,
-                            int *warps_out, const MboxArgs &mb) {
+                            int *warps_out, const MboxArgs &mb, unsigned tbase) {
     ResPlan p;
     if (!res_plan(ops, n, T, num_sms, &p, mb.on != 0)) return cudaErrorInvalidValue;
     const int64_t ns = p.wt;
     double *edges = static_cast<double *>(scratch);
-    unsigned *flags = reinterpret_cast<unsigned *>(edges + (size_t)ns * 4 * T);
+    unsigned *flags = reinterpret_cast<unsigned *>(edges + (size_t)ns * 4 * T * 2);
     cudaError_t e = cudaMemsetAsync(flags, 0, (size_t)ns * sizeof(unsigned), st);
     if (e != cudaSuccess) return e;
     int Wt = (int)p.wt;
-    // (data-as-flag: the edge slots are EMPTY already -- resident_scratch_init at create, and
-    // every completed launch leaves them so)
+    // (tagged edges need no reset between launches: tbase is new for every launch)
     void *args[] = {(void *)&A, (void *)&B, (void *)&n, (void *)&T, (void *)&nt, (void *)&q, (void *)&r,
-                    (void *)&edges, (void *)&flags, (void *)&Wt, (void *)&guard, (void *)&fr, (void *)&mb};
+                    (void *)&edges, (void *)&flags, (void *)&Wt, (void *)&guard, (void *)&fr, (void *)&mb,
+                    (void *)&tbase};
     if (warps_out) *warps_out = Wt;
     return cudaLaunchCooperativeKernel(res_fn(ops, p.rv, mb.on != 0), dim3((unsigned)p.grid),
                                        dim3((unsigned)(p.nw * 32)), args, p.smem, st);
