@@ -308,8 +308,7 @@ def kernel_roofline(info, cfg, count, world, steps, k_launches, k_ms, ms, value,
                 "unit": "TFLOP/s (4 flop/update, SURVEY §8(d))", "frac": achieved_tflops / fp64_tflops,
                 "peak_kind": pipe_kind + " x 2 flop/FMA"}
     kind = info["pass_kind"]
-    k6v = 17 if T <= 32 else 33 if T <= 64 else 49            # resident.cu rv_of(T)
-    kernel = ("k6_resident<V=%d>" % k6v if info["resident"] else
+    kernel = ("k6_resident<V=%d>" % info["resident_V"] if info["resident"] else
               "k2p_pass<V=%d,NW=%d,S=%d,KX=%d>" % (info["pass_V"], info["pass_NW"], info["pass_S"],
                                                    8 if kind == 3 else 16)) + "<OPS=%d>" % info["dp_ops"]
     # the kernel's own bound: fp64 instructions it must issue per update (dp_ops; the scaled

@@ -134,13 +134,13 @@ typedef struct {
     int64_t pad;            /* ghost cells allocated on each side of a slab                 */
     int32_t tile_cells;     /* output cells per CTA tile of the pass kernel (at T)          */
     int32_t grid;           /* CTAs per pass-kernel launch (persistent)                     */
-    int32_t pass_kind;      /* pass-kernel variant: 0 CTA tiles, 1 warp spans, 2 producer warp */
+    int32_t pass_kind;      /* pass-kernel variant: 3 / 4 = warps trading 8- / 16-deep ghosts */
     int32_t pass_V, pass_NW, pass_S; /* cells/lane, compute warps/CTA, TMA stages            */
     int32_t resident;       /* 1 if runs use the register-resident kernel K6                */
     int32_t resident_warps; /* warps of the last K6 launch                                  */
     int64_t stream_windows; /* light-cone windows of the last heat1d_solve_host (0: plain)  */
     int32_t transport;      /* HEAT1D_TRANSPORT_* in use (after create's fallback)          */
-    int32_t reserved0;
+    int32_t resident_V;     /* cells per lane of the last K6 launch (0: none yet)           */
 } heat1d_info_t;
 
 /* Exchange plan of one rank (pure host logic; usable without a GPU).  Offsets

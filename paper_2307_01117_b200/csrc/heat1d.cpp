@@ -80,6 +80,7 @@ struct heat1d_s {
     unsigned k6_tag = 1;   // edge tag of the next K6 launch's first period (resident.cu tagged words)
     void *res_scratch = nullptr;
     int res_warps = 0;
+    int res_V = 0;  // cells per lane of the last K6 launch
 
     cudaStream_t stream = nullptr, comm = nullptr;
     bool own_stream = false, own_comm = false;
@@ -264,6 +265,36 @@ int auto_T(int ops) {
     return ops == 1 ? 96 : 64;
 }
 
+// K6's period when the caller leaves T to us: every step computes all 32V
+// register cells of a span (live or slack) and every period pays one halo hand-off, about
+// 154 span-cell-steps' worth (fit to the C2/C5 A/B, profiles/r02_k6_tv.jsonl); so among
+// T in {64, 56, 48, 40} take the one minimising V(T) * nt + ceil(nt / T) * 154, V(T) the
+// plan's cells per lane for the LARGEST slab -- a global quantity, the same on every rank.
+int k6_auto_T(heat1d_t h, int64_t nx, int64_t np, int G, int64_t nt, int64_t mslab) {
+    int64_t nmax = 0;
+    for (int g = 0; g < G; ++g) {
+        int64_t f = 0, c = 0;
+        partition(nx, np, G, g, &f, &c);
+        nmax = std::max(nmax, c);
+    }
+    const int ops = h->ops_fast ? h->ops_fast : h->ops;
+    const int64_t steps = nt > 0 ? nt : 1;
+    int best = (int)std::min<int64_t>(64, mslab);
+    double best_cost = -1.0;
+    for (int T : {64, 56, 48, 40}) {
+        if (T > mslab) continue;
+        const int v = heat1d::resident_plan_v(ops, nmax, T, h->num_sms, G > 1);
+        if (v == 0) continue;
+        const double cost = (double)v * (double)steps + (double)((steps + T - 1) / T) * 154.0;
+        if (best_cost < 0 || cost < best_cost) {
+            best = T;
+            best_cost = cost;
+        }
+    }
+    cudaGetLastError();
+    return best;
+}
+
 bool parse_geom_env(PassGeom *g) {
     const char *s = getenv("HEAT1D_GEOM");  // "V,NW,S,ctas_per_sm[,kind]" (tuning knob)
     if (!s || !*s) return false;
@@ -430,7 +461,7 @@ int run_resident(heat1d_t h, int64_t nt) {
     h->k6_tag += periods + 2u;
     CK(heat1d::launch_resident(h->ops, cell0(h, s, h->cur), cell0(h, s, h->cur ^ 1), s.count, h->T, nt, h->q,
                                h->r, guard_for(h, h->ops, h->T), fast_range(h, h->ops, h->absmax), h->res_scratch,
-                               h->num_sms, h->stream, &h->res_warps, mb, tbase));
+                               h->num_sms, h->stream, &h->res_warps, &h->res_V, mb, tbase));
     h->launches++;
     rc = prof_end(h, h->stream, rec);
     if (rc) return rc;
@@ -1025,13 +1056,12 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
     if (res_ok) {
         int64_t f0 = 0, n0 = h->N;
         if (G > 1) partition(nx, np, G, o.rank, &f0, &n0);
-        // K6 period (halo refresh) <= 128; auto = 64 (V = 33 spans): half the exchanges of T = 32
-        // for +32 % (C5) / +30 % (C2) measured (profiles/r01_k6_period_sync.jsonl)
-        // (T = 64, V = 33 spans for every arithmetic form since the cross-rank mailbox code
-        // is compiled only where used: C5 matched 4114 vs 3216 GLUPS at T = 128 / V = 49;
-        // profiles/r01_k6_period_v.jsonl)
+        // K6 period (halo refresh) <= 128; auto: 40..64 by k6_auto_T (T = 32 pays twice the
+        // hand-offs for -30 %, profiles/r01_k6_period_sync.jsonl; T = 96/128 needs V = 49 spans,
+        // -25 %, profiles/r01_k6_period_v.jsonl)
         int Tr = o.T > 0 ? std::min(o.T, 128) : 64;
         if (Tr > mslab) Tr = (int)mslab;
+        if (o.T == 0) Tr = k6_auto_T(h, nx, np, G, nt, mslab);
         int coop = 0;
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
         bool fits = coop && n0 <= heat1d::resident_capacity(Tr, h->num_sms) && n0 >= Tr &&
@@ -1548,6 +1578,7 @@ int heat1d_info(heat1d_t h, heat1d_info_t *info) {
     info->pass_S = h->geom.S;
     info->resident = h->resident ? 1 : 0;
     info->resident_warps = h->res_warps;
+    info->resident_V = h->res_V;
     info->stream_windows = h->stream_windows;
     info->transport = h->transport;
     return HEAT1D_OK;

@@ -146,11 +146,12 @@ cudaError_t launch_mbox_init(double *mbox, cudaStream_t st);
 // K6: whole nt-step solve of a single-slab ring held in registers (resident.cu).
 int64_t resident_capacity(int T, int num_sms);
 bool resident_fits(int ops, int64_t n, int T, int num_sms, bool mbox = false);  // plan + co-residency
+int resident_plan_v(int ops, int64_t n, int T, int num_sms, bool mbox);  // cells per lane of the plan, 0: no fit
 size_t resident_scratch_bytes(int T, int num_sms);
 cudaError_t resident_scratch_init(void *scratch, int T, int num_sms, cudaStream_t st);
 cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
                             double r, Guard guard, const FastRange &fr, void *scratch, int num_sms, cudaStream_t st,
-                            int *warps_out, const MboxArgs &mb,
+                            int *warps_out, int *v_out, const MboxArgs &mb,
                             unsigned tbase);  // tag of this launch's first period (>= 1, new per launch)
 
 }  // namespace heat1d

@@ -500,10 +500,14 @@ k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int
 }
 
 namespace {
-// cells per lane: 17 for periods T <= 32, 33 for 32 < T <= 64, 49 up to 128 (span 32V >= own + 2T)
+// cells per lane: at most 17 for periods T <= 32, 33 for 32 < T <= 64, 49 up to 128 (span
+// 32V >= own + 2T); the plan then takes the smallest instantiated V that holds its spans
+// (every step computes all 32V register cells, live or slack: C2's 845-cell spans + 128 halo
+// cells fit V = 31, 6 % less work than V = 33)
 int rv_of(int T) { return T > 64 ? 49 : T > 32 ? 33 : 17; }
-// warps per SM the register budget allows: V=17: ~100 regs; V=33: ~128 regs; V=49: ~220 regs
-int max_wps(int rv) { return rv == 49 ? 9 : rv == 33 ? 15 : 20; }
+constexpr int kResV[] = {17, 25, 29, 31, 33, 49};  // instantiated (res_fn)
+// warps per SM the register budget allows: V=17: ~100 regs; V=25..33: <= 128 regs; V=49: ~220 regs
+int max_wps(int rv) { return rv == 49 ? 9 : rv >= 25 ? 15 : 20; }
 constexpr int MAX_WPS_ANY = 20;
 constexpr int MAX_NW = 8;     // warps per CTA (__launch_bounds__(256))
 
@@ -517,11 +521,11 @@ struct ResPlan {
 // compiled with a 2-blocks/SM register target: left alone ptxas gave them ~155 registers
 // and -25 %; profiles/r01_k6_sync3.jsonl).  V = 17 spans (periods T <= 32) keep the flag
 // protocol, whose build keeps three CTAs per SM co-resident for the largest on-chip rings.
-bool res_df(int rv) { return rv >= 33; }
+bool res_df(int rv) { return rv >= 25; }
 
 template <int V>
 const void *res_fn_v(int ops, bool mbox) {
-    constexpr bool DF = V >= 33;
+    constexpr bool DF = V >= 25;
     if (mbox) {
         switch (ops) {
             case 4: return (const void *)&k6_resident<V, 4, true, DF>;
@@ -539,7 +543,14 @@ const void *res_fn_v(int ops, bool mbox) {
 }
 
 const void *res_fn(int ops, int rv, bool mbox) {
-    return rv == 49 ? res_fn_v<49>(ops, mbox) : rv == 33 ? res_fn_v<33>(ops, mbox) : res_fn_v<17>(ops, mbox);
+    switch (rv) {
+        case 49: return res_fn_v<49>(ops, mbox);
+        case 33: return res_fn_v<33>(ops, mbox);
+        case 31: return res_fn_v<31>(ops, mbox);
+        case 29: return res_fn_v<29>(ops, mbox);
+        case 25: return res_fn_v<25>(ops, mbox);
+        default: return res_fn_v<17>(ops, mbox);
+    }
 }
 
 cudaError_t res_attr(const void *fn) {  // raise the dynamic shared-memory limit once per kernel
@@ -580,16 +591,25 @@ bool res_plan(int ops, int64_t n, int T, int num_sms, ResPlan *p, bool mbox = fa
         p->grid = p->wt;
     }
     const int64_t ns = p->wt;
-    if (n / ns < T || n / ns + (n % ns ? 1 : 0) + 2 * T > 32 * RV) return false;
-    p->smem = (size_t)p->nw * (32 * RV + 1) * sizeof(double);
-    const void *fn = res_fn(ops, RV, mbox);
+    const int64_t need = n / ns + (n % ns ? 1 : 0) + 2 * T;  // the largest span with its halos
+    if (n / ns < T || need > 32 * RV) return false;
+#ifndef HEAT1D_K6_VFIXED
+    // the smallest V of the same protocol family (flags: 17; tagged words: 25..49) that holds it
+    for (int v : kResV)
+        if (v <= RV && res_df(v) == res_df(RV) && 32 * v >= need) {
+            p->rv = v;
+            break;
+        }
+#endif
+    p->smem = (size_t)p->nw * (32 * p->rv + 1) * sizeof(double);
+    const void *fn = res_fn(ops, p->rv, mbox);
     if (res_attr(fn) != cudaSuccess) return false;
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, (int)(p->nw * 32), p->smem) != cudaSuccess)
         return false;
     if (getenv("HEAT1D_DEBUG"))
         fprintf(stderr, "[heat1d] K6 plan n=%lld T=%d V=%d ops=%d wt=%lld nw=%lld grid=%lld occ=%d smem=%zu\n",
-                (long long)n, T, RV, ops, (long long)p->wt, (long long)p->nw, (long long)p->grid, occ, p->smem);
+                (long long)n, T, p->rv, ops, (long long)p->wt, (long long)p->nw, (long long)p->grid, occ, p->smem);
     return (int64_t)occ * num_sms >= p->grid;  // cooperative launch: all CTAs co-resident
 }
 
@@ -603,6 +623,11 @@ int64_t resident_capacity(int T, int num_sms) {
 bool resident_fits(int ops, int64_t n, int T, int num_sms, bool mbox) {
     ResPlan p;
     return res_plan(ops, n, T, num_sms, &p, mbox);
+}
+
+int resident_plan_v(int ops, int64_t n, int T, int num_sms, bool mbox) {
+    ResPlan p;
+    return res_plan(ops, n, T, num_sms, &p, mbox) ? p.rv : 0;
 }
 
 __global__ void k6_fill_empty(double *edges, int64_t count) {
@@ -632,7 +657,7 @@ cudaError_t launch_mbox_init(double *mbox, cudaStream_t st) {  // every data slo
 
 cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
                             double r, Guard guard, const FastRange &fr, void *scratch, int num_sms, cudaStream_t st,
-                            int *warps_out, const MboxArgs &mb, unsigned tbase) {
+                            int *warps_out, int *v_out, const MboxArgs &mb, unsigned tbase) {
     ResPlan p;
     if (!res_plan(ops, n, T, num_sms, &p, mb.on != 0)) return cudaErrorInvalidValue;
     const int64_t ns = p.wt;
@@ -646,6 +671,7 @@ cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int 
                     (void *)&edges, (void *)&flags, (void *)&Wt, (void *)&guard, (void *)&fr, (void *)&mb,
                     (void *)&tbase};
     if (warps_out) *warps_out = Wt;
+    if (v_out) *v_out = p.rv;
     return cudaLaunchCooperativeKernel(res_fn(ops, p.rv, mb.on != 0), dim3((unsigned)p.grid),
                                        dim3((unsigned)(p.nw * 32)), args, p.smem, st);
 }

@@ -88,7 +88,7 @@ class Info(ctypes.Structure):
         ("resident_warps", ctypes.c_int32),
         ("stream_windows", ctypes.c_int64),
         ("transport", ctypes.c_int32),
-        ("reserved0", ctypes.c_int32),
+        ("resident_V", ctypes.c_int32),
     ]
 
 
