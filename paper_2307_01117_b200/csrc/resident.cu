@@ -11,7 +11,7 @@
 //
 // Synchronisation is pairwise, no grid-wide barrier: spans of V = 17 cells per
 // lane (periods T <= 32) publish their edges with a release of a per-span flag;
-// spans of V >= 33 (the default period T = 64) publish tagged words (below): no
+// spans of V >= 25 (periods 32 < T <= 128) publish tagged words (below): no
 // flag, no fence.  Edge buffers are double-buffered by period parity: a span
 // writes period p+2 edges only after its neighbours published p+1, i.e. after
 // they finished reading period p.
@@ -197,7 +197,7 @@ __device__ __forceinline__ void regs_to_row(const double (&u)[V], double *row, i
     __syncwarp();
 }
 
-// Sync mode 3 ("the data is the flag"): an edge slot holds HEAT1D_EMPTY -- a signalling
+// Mailboxes between ranks ("the data is the flag"): a slot holds HEAT1D_EMPTY -- a signalling
 // NaN, which no fp64 arithmetic result can be (arithmetic returns quiet NaNs), and every
 // published edge value is an arithmetic result -- until its producer writes it; the
 // consumer polls the values themselves (one L2 round trip instead of release, poll and
@@ -234,7 +234,7 @@ __device__ __forceinline__ void fence_acq_rel() {
 // arithmetic on either NaN gives the same canonical NaN)
 constexpr unsigned long long HEAT1D_EMPTY_QUIET = HEAT1D_EMPTY | (1ull << 51);
 
-// Tagged words (the spans' edges inside one GPU, V >= 33): an edge value travels as two
+// Tagged words (the spans' edges inside one GPU, V >= 25): an edge value travels as two
 // 8-byte words (tag << 32) | half, stored by one st.v2.b64.  Each naturally aligned 8-byte
 // element of a vector access is single-copy atomic (PTX memory model), so a reader that
 // finds the expected tag in both words holds both halves of that one write.  Tags are
@@ -262,7 +262,7 @@ __device__ __forceinline__ unsigned long long *tagged_slot(double *edges, int id
 }
 
 // edges: [Ns][2 parities][2 sides][T]; publish this span's period-p edges
-// (DF: data-as-flag protocol, compiled into its own kernel instantiation)
+// (DF: tagged words, compiled into its own kernel instantiation; else a release flag per span)
 template <bool DF = false>
 __device__ __forceinline__ void publish(const Span &s, int T, unsigned p, double *edges, unsigned *flags,
                                         unsigned tbase, int lane) {
@@ -333,7 +333,7 @@ __device__ __forceinline__ void mbox_publish(const Span &s, int Ns, int T, unsig
 // on, the slab's outer halos come from the neighbour ranks (exchange index g)
 // initial: the exchange of the initial state (only the remote sides; the local halos
 // were loaded from the slab).
-// Halo refresh of a V >= 33 span, kept out of line: inlined into the period loop its 64-bit
+// Halo refresh of a V >= 25 span, kept out of line: inlined into the period loop its 64-bit
 // polls and pointers raised the matched kernels from 115 to 154 registers (and -25 %).
 // A side is either tagged (a neighbour span on this GPU: L2/R2, expected tag `tag`) or a
 // data-as-flag mailbox slot (a neighbour rank: LE/RE, EMPTY until written, reset by us).
@@ -441,7 +441,7 @@ __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, double
 }  // namespace
 
 // MB: the cross-rank mailbox code is compiled in (only then: it costs ~30 registers).
-// DF: data-as-flag halos (V >= 33 spans).
+// DF: tagged-word halos between spans (V >= 25), data-as-flag mailboxes between ranks.
 template <int V, int OPS, bool MB, bool DF>
 __global__ void __launch_bounds__(256, (DF && V <= 33 && !(MB && OPS == 1)) ? 2 : 0)
 k6_resident(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t nt, double r,
@@ -517,7 +517,7 @@ struct ResPlan {
     size_t smem = 0;
 };
 
-// Data-as-flag halos for V >= 33 spans (every arithmetic form; the matched kernels are
+// Tagged-word halos for V >= 25 spans (every arithmetic form; the matched kernels are
 // compiled with a 2-blocks/SM register target: left alone ptxas gave them ~155 registers
 // and -25 %; profiles/r01_k6_sync3.jsonl).  V = 17 spans (periods T <= 32) keep the flag
 // protocol, whose build keeps three CTAs per SM co-resident for the largest on-chip rings.
