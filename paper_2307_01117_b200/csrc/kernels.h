@@ -127,12 +127,13 @@ cudaError_t launch_absmax(const double *u, int64_t count, unsigned long long *ou
 cudaError_t launch_init_uniform(double *u, int64_t count, int64_t first, uint64_t seed,
                                 double lo, double hi, cudaStream_t st);
 
-// K6 across ranks: each rank's mailbox = double[2 sides][2 slots][MBOX_TMAX] + two flag
+// K6 across ranks: each rank's mailbox = [2 sides][2 slots][MBOX_TMAX] cells of 16 bytes (two
+// tagged words, resident.cu; the V = 17 flag protocol uses them as plain doubles) + two flag
 // words on their own 128-byte lines at MBOX_FLAG_OFF (side 0: from the left rank, side 1:
 // from the right rank).  left/right point at the neighbour ranks' mailboxes (CUDA IPC peer
 // mappings over NVLink; == self for one rank, which routes the ring's wrap through them).
 constexpr int MBOX_TMAX = 128;
-constexpr size_t MBOX_FLAG_OFF = 2 * 2 * MBOX_TMAX * sizeof(double);
+constexpr size_t MBOX_FLAG_OFF = 2 * 2 * MBOX_TMAX * 16;
 constexpr size_t MBOX_BYTES = MBOX_FLAG_OFF + 256;
 struct MboxArgs {
     double *self = nullptr, *left = nullptr, *right = nullptr;
@@ -140,7 +141,7 @@ struct MboxArgs {
     int on = 0;
 };
 
-// Initialise a mailbox: data slots to the data-as-flag EMPTY pattern, flag words to 0.
+// Initialise a mailbox: every data word tag 0 (never a live tag), flag words 0.
 cudaError_t launch_mbox_init(double *mbox, cudaStream_t st);
 
 // K6: whole nt-step solve of a single-slab ring held in registers (resident.cu).

@@ -197,62 +197,37 @@ __device__ __forceinline__ void regs_to_row(const double (&u)[V], double *row, i
     __syncwarp();
 }
 
-// Mailboxes between ranks ("the data is the flag"): a slot holds HEAT1D_EMPTY -- a signalling
-// NaN, which no fp64 arithmetic result can be (arithmetic returns quiet NaNs), and every
-// published edge value is an arithmetic result -- until its producer writes it; the
-// consumer polls the values themselves (one L2 round trip instead of release, poll and
-// two acquires), takes them and writes EMPTY back.  A fence before each publish orders
-// those resets before the data that lets the producer reuse the slot two periods later
-// (PTX fence-fence synchronisation through the observed values).
-constexpr unsigned long long HEAT1D_EMPTY = 0x7ff0dead00000001ull;
-
-// SYS: system scope (mailboxes written by a peer GPU over NVLink), else GPU scope.
+// Tagged words (V >= 25: the spans' edges inside one GPU, and the mailboxes between ranks):
+// an edge value travels as two 8-byte words (tag << 32) | half, stored by one st.v2.b64.
+// Each naturally aligned 8-byte element of a vector access is single-copy atomic (PTX
+// memory model; over NVLink as well -- NCCL's LL protocol rests on the same property), so a
+// reader that finds the expected tag in both words holds both halves of that one write.
+// Tags are unique per launch and period (spans: tbase + p, the host advances tbase past every
+// launch; mailboxes: the global exchange index + 1), so a slot's stale content never matches;
+// the reader writes nothing back and nobody fences: a slot is overwritten (two periods later)
+// only after its writer computed from the reader's next edges, which the reader computed from
+// the values it read (a data dependency orders its read before its next publish).
+// SYS: system scope (a neighbour rank's mailbox over NVLink), else GPU scope.
 template <bool SYS = false>
-__device__ __forceinline__ void st_relaxed_u64(double *p, double v) {
-    if constexpr (SYS)
-        asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)) : "memory");
-    else
-        asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)) : "memory");
-}
-template <bool SYS = false>
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const double *p) {
-    unsigned long long v;
-    if constexpr (SYS)
-        asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    else
-        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-template <bool SYS = false>
-__device__ __forceinline__ void fence_acq_rel() {
-    if constexpr (SYS)
-        asm volatile("fence.acq_rel.sys;" ::: "memory");
-    else
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-}
-// an initial-state value that happens to be the EMPTY pattern is sent quieted (fp64
-// arithmetic on either NaN gives the same canonical NaN)
-constexpr unsigned long long HEAT1D_EMPTY_QUIET = HEAT1D_EMPTY | (1ull << 51);
-
-// Tagged words (the spans' edges inside one GPU, V >= 25): an edge value travels as two
-// 8-byte words (tag << 32) | half, stored by one st.v2.b64.  Each naturally aligned 8-byte
-// element of a vector access is single-copy atomic (PTX memory model), so a reader that
-// finds the expected tag in both words holds both halves of that one write.  Tags are
-// unique per launch and period (tbase + p, the host advances tbase past every launch), so a
-// slot's stale content never matches; the reader writes nothing back and nobody fences:
-// a span overwrites a slot (period p+2) only after computing from its neighbour's period
-// p+1 edges, which that neighbour computed from the period-p values it read (a data
-// dependency orders its read before its next publish).
 __device__ __forceinline__ void st_tagged(unsigned long long *p, double v, unsigned tag) {
     const unsigned long long b = (unsigned long long)__double_as_longlong(v);
     const unsigned long long t = (unsigned long long)tag << 32;
-    asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(t | (b & 0xffffffffull)),
-                 "l"(t | (b >> 32))
-                 : "memory");
+    if constexpr (SYS)
+        asm volatile("st.relaxed.sys.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(t | (b & 0xffffffffull)),
+                     "l"(t | (b >> 32))
+                     : "memory");
+    else
+        asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(t | (b & 0xffffffffull)),
+                     "l"(t | (b >> 32))
+                     : "memory");
 }
+template <bool SYS = false>
 __device__ __forceinline__ bool ld_tagged(const unsigned long long *p, unsigned tag, double *v) {
     unsigned long long w0, w1;
-    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+    if constexpr (SYS)
+        asm volatile("ld.relaxed.sys.global.v2.b64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+    else
+        asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
     *v = __longlong_as_double((long long)((w1 << 32) | (w0 & 0xffffffffull)));
     return (unsigned)(w0 >> 32) == tag && (unsigned)(w1 >> 32) == tag;
 }
@@ -289,30 +264,29 @@ __device__ __forceinline__ void publish(const Span &s, int T, unsigned p, double
 // with remote (NVLink) stores and a system-scope release of the slot's flag; each rank
 // reads its own mailbox.  Slots alternate with the global exchange index g (see
 // launch_resident: indices never repeat across runs, and skip one at run boundaries).
-__device__ __forceinline__ double *mbox_data(double *mb, int side, unsigned g) {
-    return mb + ((size_t)side * 2 + (g & 1)) * MBOX_TMAX;
+__device__ __forceinline__ double *mbox_data(double *mb, int side, unsigned g) {  // 2 doubles per cell
+    return mb + ((size_t)side * 2 + (g & 1)) * MBOX_TMAX * 2;
+}
+__device__ __forceinline__ unsigned long long *mbox_tagged(double *mb, int side, unsigned g) {
+    return reinterpret_cast<unsigned long long *>(mbox_data(mb, side, g));
 }
 __device__ __forceinline__ unsigned *mbox_flag(double *mb, int side) {
     return reinterpret_cast<unsigned *>(reinterpret_cast<char *>(mb) + MBOX_FLAG_OFF) + side * 32;
 }
 
-// DF: data-as-flag across GPUs -- the values go straight into the neighbour's mailbox
-// slot (EMPTY until written, reset by its reader), no flag; the fence orders this rank's
-// earlier resets of its own mailbox before the data that lets the neighbour reuse them.
+// DF: tagged words straight into the neighbour rank's mailbox slot (tag g + 1), no flag, no
+// fence; else the slot's values plus a system-scope release of its flag.
 template <bool DF = false>
 __device__ __forceinline__ void mbox_publish(const Span &s, int Ns, int T, unsigned g, const MboxArgs &mb, int lane) {
     if constexpr (DF) {
-        fence_acq_rel<true>();
-        auto put = [&](double *D, const double *src) {
-            for (int i = lane; i < T; i += 32) {
-                double x = src[i];
-                if ((unsigned long long)__double_as_longlong(x) == HEAT1D_EMPTY)
-                    x = __longlong_as_double((long long)HEAT1D_EMPTY_QUIET);
-                st_relaxed_u64<true>(D + i, x);
-            }
-        };
-        if (s.id == 0) put(mbox_data(mb.left, 1, g), s.row + T);
-        if (s.id == Ns - 1) put(mbox_data(mb.right, 0, g), s.row + s.own);
+        if (s.id == 0) {
+            unsigned long long *D = mbox_tagged(mb.left, 1, g);
+            for (int i = lane; i < T; i += 32) st_tagged<true>(D + 2 * i, s.row[T + i], g + 1);
+        }
+        if (s.id == Ns - 1) {
+            unsigned long long *D = mbox_tagged(mb.right, 0, g);
+            for (int i = lane; i < T; i += 32) st_tagged<true>(D + 2 * i, s.row[s.own + i], g + 1);
+        }
         return;
     }
     if (s.id == 0) {
@@ -335,13 +309,13 @@ __device__ __forceinline__ void mbox_publish(const Span &s, int Ns, int T, unsig
 // were loaded from the slab).
 // Halo refresh of a V >= 25 span, kept out of line: inlined into the period loop its 64-bit
 // polls and pointers raised the matched kernels from 115 to 154 registers (and -25 %).
-// A side is either tagged (a neighbour span on this GPU: L2/R2, expected tag `tag`) or a
-// data-as-flag mailbox slot (a neighbour rank: LE/RE, EMPTY until written, reset by us).
-// doL/doR false: that side's halo is already valid (the initial exchange of local sides).
+// Each side is a neighbour span's tagged edge on this GPU (gpu scope, tag tl / tr) or, with
+// SYS, this rank's mailbox slot filled by a neighbour rank (system scope); null = that side's
+// halo is already valid (the initial exchange of local sides).
 template <bool SYS>
-__device__ __noinline__ void refresh_df(double *row, int own, int T, const unsigned long long *L2,
-                                        const unsigned long long *R2, double *LE, double *RE, bool doL, bool doR,
-                                        unsigned tag, int lane) {
+__device__ __noinline__ void refresh_df(double *row, int own, int T, const unsigned long long *L,
+                                        const unsigned long long *R, bool lsys, bool rsys, unsigned tl, unsigned tr,
+                                        int lane) {
     const unsigned long long t0 = SYS ? globaltimer_ns() : 0;
     for (int i0 = 0; i0 < T; i0 += 32) {
         const int i = i0 + lane;
@@ -350,37 +324,15 @@ __device__ __noinline__ void refresh_df(double *row, int own, int T, const unsig
         do {
             bool lok = true, rok = true;
             if (i < T) {
-                if (doL) {
-                    if (L2) {
-                        lok = ld_tagged(L2 + 2 * i, tag, &lv);
-                    } else {
-                        const unsigned long long l = ld_relaxed_u64<SYS>(LE + i);
-                        lok = l != HEAT1D_EMPTY;
-                        lv = __longlong_as_double((long long)l);
-                    }
-                }
-                if (doR) {
-                    if (R2) {
-                        rok = ld_tagged(R2 + 2 * i, tag, &rv);
-                    } else {
-                        const unsigned long long rr = ld_relaxed_u64<SYS>(RE + i);
-                        rok = rr != HEAT1D_EMPTY;
-                        rv = __longlong_as_double((long long)rr);
-                    }
-                }
+                if (L) lok = (SYS && lsys) ? ld_tagged<true>(L + 2 * i, tl, &lv) : ld_tagged<false>(L + 2 * i, tl, &lv);
+                if (R) rok = (SYS && rsys) ? ld_tagged<true>(R + 2 * i, tr, &rv) : ld_tagged<false>(R + 2 * i, tr, &rv);
             }
             ok = lok && rok;
             if (SYS && globaltimer_ns() - t0 > HEAT1D_WAIT_NS) __trap();  // a neighbour rank is gone
         } while (!__all_sync(0xffffffffu, ok));
         if (i < T) {
-            if (doL) {
-                row[i] = lv;
-                if (!L2) st_relaxed_u64<SYS>(LE + i, __longlong_as_double((long long)HEAT1D_EMPTY));
-            }
-            if (doR) {
-                row[own + T + i] = rv;
-                if (!R2) st_relaxed_u64<SYS>(RE + i, __longlong_as_double((long long)HEAT1D_EMPTY));
-            }
+            if (L) row[i] = lv;
+            if (R) row[own + T + i] = rv;
         }
     }
     __syncwarp();
@@ -393,10 +345,10 @@ __device__ __forceinline__ void refresh(const Span &s, int T, unsigned p, double
     const bool lrem = mb.on && s.id == 0, rrem = mb.on && s.id == Ns - 1;
     if constexpr (DF) {
         // left neighbour's side 1 and right neighbour's side 0, or this rank's mailbox
-        refresh_df<SYS>(s.row, s.own, T, lrem ? nullptr : tagged_slot(edges, s.left, p & 1, 1, T),
-                        rrem ? nullptr : tagged_slot(edges, s.right, p & 1, 0, T),
-                        lrem ? mbox_data(mb.self, 0, g) : nullptr, rrem ? mbox_data(mb.self, 1, g) : nullptr,
-                        lrem || !initial, rrem || !initial, tbase + p, lane);
+        const unsigned long long *L = lrem ? mbox_tagged(mb.self, 0, g) : tagged_slot(edges, s.left, p & 1, 1, T);
+        const unsigned long long *R = rrem ? mbox_tagged(mb.self, 1, g) : tagged_slot(edges, s.right, p & 1, 0, T);
+        refresh_df<SYS>(s.row, s.own, T, (lrem || !initial) ? L : nullptr, (rrem || !initial) ? R : nullptr, lrem,
+                        rrem, lrem ? g + 1 : tbase + p, rrem ? g + 1 : tbase + p, lane);
         return;
     }
     if (lrem || rrem) {
@@ -630,11 +582,6 @@ int resident_plan_v(int ops, int64_t n, int T, int num_sms, bool mbox) {
     return res_plan(ops, n, T, num_sms, &p, mbox) ? p.rv : 0;
 }
 
-__global__ void k6_fill_empty(double *edges, int64_t count) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
-        edges[i] = __longlong_as_double((long long)HEAT1D_EMPTY);
-}
-
 // edges: [Ns][2 parities][2 sides][T] cells, 16 B each (tagged words; the V = 17 flag
 // protocol uses the first half as plain doubles), then the per-span flags
 size_t resident_scratch_bytes(int T, int num_sms) {
@@ -648,11 +595,8 @@ cudaError_t resident_scratch_init(void *scratch, int T, int num_sms, cudaStream_
 }
 
 
-cudaError_t launch_mbox_init(double *mbox, cudaStream_t st) {  // every data slot EMPTY, flags 0
-    cudaError_t e = cudaMemsetAsync(mbox, 0, MBOX_BYTES, st);
-    if (e != cudaSuccess) return e;
-    k6_fill_empty<<<4, 128, 0, st>>>(mbox, (int64_t)(MBOX_FLAG_OFF / sizeof(double)));
-    return cudaGetLastError();
+cudaError_t launch_mbox_init(double *mbox, cudaStream_t st) {  // every tag 0, flags 0
+    return cudaMemsetAsync(mbox, 0, MBOX_BYTES, st);
 }
 
 cudaError_t launch_resident(int ops, const double *A, double *B, int64_t n, int T, int64_t nt, double q,
