@@ -1179,6 +1179,10 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
         h->mbox_left = h->mbox_right = h->mbox;
     }
     if (const char *dl = getenv("HEAT1D_COMM_DELAY_US")) h->comm_delay_us = (unsigned)atoi(dl);
+    if (const char *k0 = getenv("HEAT1D_K6_COUNTER0")) {  // test hook: K6 tag / exchange counters start
+        h->k6_tag = h->k6_base = (unsigned)strtoul(k0, nullptr, 0);  // here (near 2^32: the wrap path)
+        if (h->k6_tag == 0) h->k6_tag = 1;
+    }
     if (const char *pp = getenv("HEAT1D_POISON_PADS")) h->poison_pads = atoi(pp) == 1;
     // HEAT1D_GEOM (tuning knob) only where the pass kernel exists for every arithmetic variant
     // this handle may run (its matched/fast form and the 3-op fallback); else the default

@@ -921,3 +921,23 @@ def test_trace_shows_halo_work_beside_the_interior(h1, transport):
         ks = k2[i * G:(i + 1) * G]
         assert all(e[3] >= e[2] >= 0 for e in ks) and hv[3] >= hv[2] >= 0
         assert hv[2] < max(e[3] for e in ks)   # the halo work starts while the interior runs
+
+
+@pytest.mark.parametrize("mailbox", [False, True])
+def test_resident_tag_counters_wrap(h1, monkeypatch, mailbox):
+    """K6's halo tags are 32-bit counters (tagged words, resident.cu): started just below 2^32
+    (test hook HEAT1D_K6_COUNTER0), a sequence of runs crosses the wrap -- the span tags restart
+    with freshly zeroed slots, the mailbox tags (exchange index + 1) wrap through 0 -- and stays
+    bitwise equal to the oracle."""
+    monkeypatch.setenv("HEAT1D_K6_COUNTER0", str(2 ** 32 - 20))  # the 4th run crosses 2^32
+    if mailbox:
+        monkeypatch.setenv("HEAT1D_K6_MAILBOX", "1")
+    N, T = 300_007, 64
+    u0 = synth.uniform(5, 0, N, -1.0, 1.0)
+    with h1.Heat1D(N, 1, 0, 0.5, 1.0, 1.0, T=T, resident=True) as h:
+        h.set_initial(u0)
+        want = u0
+        for nt in (5 * T + 3, 1, 2 * T, 7 * T + 11, T + 1, 3 * T):
+            h.run(nt)
+            want = oracle.run(want, 0.5, nt)
+            assert_bitwise(h.get(), want, "tags across the wrap, mailbox=%s nt=%d" % (mailbox, nt))
