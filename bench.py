@@ -309,8 +309,9 @@ def kernel_roofline(info, cfg, count, world, steps, k_launches, k_ms, ms, value,
                 "peak_kind": pipe_kind + " x 2 flop/FMA"}
     kind = info["pass_kind"]
     kernel = ("k6_resident<V=%d>" % info["resident_V"] if info["resident"] else
-              "k2p_pass<V=%d,NW=%d,S=%d,KX=%d>" % (info["pass_V"], info["pass_NW"], info["pass_S"],
-                                                   8 if kind == 3 else 16)) + "<OPS=%d>" % info["dp_ops"]
+              "%s<V=%d,NW=%d,S=%d,KX=%d>" % ("k2f_pass" if info.get("pass_feed") else "k2p_pass", info["pass_V"],
+                                             info["pass_NW"], info["pass_S"], 8 if kind == 3 else 16)) + \
+        "<OPS=%d>" % info["dp_ops"]
     # the kernel's own bound: fp64 instructions it must issue per update (dp_ops; the scaled
     # fast variants add one rescale DMUL per cell per pass) against the fp64 pipe's issue rate
     inst_per_upd = info["dp_ops"] + (1.0 / steps_per_pass if info["dp_ops"] <= 2 else 0.0)

@@ -141,6 +141,8 @@ typedef struct {
     int64_t stream_windows; /* light-cone windows of the last heat1d_solve_host (0: plain)  */
     int32_t transport;      /* HEAT1D_TRANSPORT_* in use (after create's fallback)          */
     int32_t resident_V;     /* cells per lane of the last K6 launch (0: none yet)           */
+    int32_t pass_feed;      /* 1: full passes run feed tiles (k2f_pass: strips, left-fed tiles) */
+    int32_t reserved1;
 } heat1d_info_t;
 
 /* Exchange plan of one rank (pure host logic; usable without a GPU).  Offsets

@@ -256,13 +256,15 @@ end:
     return e != ncclSuccess ? e : e2;
 }
 
-int auto_T(int ops) {
-    // DESIGN.md §6 (T sweeps in profiles/r01_sweep_kx.jsonl, r01_c3_tsweep.md): each pass
-    // moves 16/T bytes per update, so T is raised until the pass is fp64-issue bound; with
-    // the inter-warp ghost exchange (kind 4) the extra work of a deeper pass is only the
-    // CTA-edge trapezoid 2T/(NW 32V).  T = 64 is within 1 % of the best measured T for the
-    // 2-, 3- and 4-op forms; the 1-op form (fast, r = 1/2) gains another 1.8 % at T = 96.
-    return ops == 1 ? 96 : 64;
+int auto_T(int ops, double r) {
+    // each pass moves 16/T bytes per update, so T is raised until the pass is
+    // fp64-issue bound; what a deeper pass costs is redundant cells -- with feed tiles
+    // (k2f_pass) only the right margin, T^2/2 cell-steps per tile -- against per-tile phases
+    // that a deeper pass amortises: T = 128, the largest, is the fastest for every arithmetic
+    // form (profiles/r02_feed_ab.md).  The scaled 2-op form grows by r^-T within a pass, so
+    // it takes 128 only while r^-128 <= 2^512 (r >= 1/16), else 64 (r >= 1/256: <= 2^512).
+    if (ops == 2 && r < 1.0 / 16.0) return 64;
+    return 128;
 }
 
 // K6's period when the caller leaves T to us: every step computes all 32V
@@ -1036,7 +1038,7 @@ int heat1d_create(heat1d_t *out, int64_t nx, int64_t np, int64_t nt, double k, d
 
     // T and the kernel family.  K2 passes: T from opts or auto_T, clamped to
     // the smallest slab (and half of it for the P2P edge strips) -- the same on every rank.
-    int T = o.T > 0 ? o.T : auto_T(h->ops_fast ? h->ops_fast : h->ops);
+    int T = o.T > 0 ? o.T : auto_T(h->ops_fast ? h->ops_fast : h->ops, r);
     if (o.kernel == HEAT1D_KERNEL_NAIVE) T = 1;
     if (T > mslab) T = (int)mslab;  // a slab must hold its own halo
     if (o.transport == HEAT1D_TRANSPORT_P2P && G > 1) {
@@ -1583,6 +1585,7 @@ int heat1d_info(heat1d_t h, heat1d_info_t *info) {
     info->resident = h->resident ? 1 : 0;
     info->resident_warps = h->res_warps;
     info->resident_V = h->res_V;
+    info->pass_feed = heat1d::pass_uses_feed(h->geom, h->ops_fast ? h->ops_fast : h->ops, h->T) ? 1 : 0;
     info->stream_windows = h->stream_windows;
     info->transport = h->transport;
     return HEAT1D_OK;

@@ -16,6 +16,7 @@
 // ghost zones.  The arithmetic is stencil.cuh; DESIGN.md §6
 // describes the data layout and the roofline of each kernel.
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <mutex>
 
@@ -414,11 +415,307 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
     }
 }
 
+// ------------------------------------------------------------------ K2f: feed tiles
+//
+// k2f_pass: K2 with each CTA walking a contiguous STRIP of the output, tile after tile,
+// where every tile but the strip's first is fed its left boundary: the previous tile's last
+// warp records, at every step t, the time-t value of the cell just left of the next tile
+// (one column, shared memory), and the next tile's warp 0 lane 0 takes its left neighbour
+// at step t from that record instead of computing a T-deep left halo.  So only the right
+// side keeps a shrinking margin: T^2/2 wasted cell-steps per tile instead of 2 T^2 (K2's
+// two trapezoids), and a tile's output grows from SPAN - 2T to SPAN - T cells.  (A parallel-
+// ogram tiling: each tile's output is its window shifted left by T at the end of the pass.)
+// T is a template parameter (the recorded column's lane and register are compile-time);
+// other T, tail passes and other geometries run k2p_pass.
+//
+// Exactness guard: the fed values of a tile depend on time-0 cells of the previous tile's
+// window (the cone of the recorded column, < T cells back), so a tile takes the contracted
+// form only if its own cells AND the previous tile's cells passed the guard.
+template <int V, int OPS, int LS, int JS>
+__device__ __forceinline__ void warp_step_fd(const double (&u)[V], double (&v)[V], double r, int t, const double *fin,
+                                             double *fout, bool rd, bool wr, int lane) {
+    if (wr && lane == LS) fout[t] = u[JS];  // the time-t value of the next tile's left neighbour
+    double L = __shfl_up_sync(0xffffffffu, u[V - 1], 1);
+    const double R = __shfl_down_sync(0xffffffffu, u[0], 1);
+    if (rd && lane == 0) L = fin[t];
+#pragma unroll
+    for (int j = 1; j < V - 1; ++j) v[j] = eq2<OPS>(u[j - 1], u[j], u[j + 1], r);
+    v[0] = eq2<OPS>(L, u[0], u[1], r);
+    v[V - 1] = eq2<OPS>(u[V - 2], u[V - 1], R, r);
+}
+
+template <int V, int OPS, int LS, int JS, int N>
+__device__ __forceinline__ void warp_steps_fd_fixed(double (&u)[V], double r, int t0, const double *fin,
+                                                    double *fout, bool rd, bool wr, int lane) {
+    double v[V];
+#pragma unroll
+    for (int s = 0; s < N; s += 2) {
+        warp_step_fd<V, OPS, LS, JS>(u, v, r, t0 + s, fin, fout, rd, wr, lane);
+        warp_step_fd<V, OPS, LS, JS>(v, u, r, t0 + s + 1, fin, fout, rd, wr, lane);
+    }
+}
+
+template <int V, int OPS, int LS, int JS>
+__device__ __forceinline__ void warp_steps_fd(double (&u)[V], int K, double r, int t0, const double *fin,
+                                              double *fout, bool rd, bool wr, int lane) {
+    double v[V];
+    int s = 0;
+    for (; s + 2 <= K; s += 2) {
+        warp_step_fd<V, OPS, LS, JS>(u, v, r, t0 + s, fin, fout, rd, wr, lane);
+        warp_step_fd<V, OPS, LS, JS>(v, u, r, t0 + s + 1, fin, fout, rd, wr, lane);
+    }
+    if (s < K) {
+        warp_step_fd<V, OPS, LS, JS>(u, v, r, t0 + s, fin, fout, rd, wr, lane);
+#pragma unroll
+        for (int j = 0; j < V; ++j) u[j] = v[j];
+    }
+}
+
+// The TT steps of a tile (tile_steps with the feed hooks).  prev_ok: the previous tile's
+// guard verdict (CTA-uniform); own_ok returns this tile's (for the next).
+template <int V, int NW, int KX, int OPS, bool GUARD, int TT>
+__device__ __forceinline__ bool tile_steps_fd(double (&u)[V], double r, double scale, double *xbuf,
+                                              const double *fin, double *fout, bool rd, int warp, int lane,
+                                              bool ok, bool prev_ok, bool &own_ok) {
+    constexpr int POS = 32 * V - TT - 1;  // the recorded column in the last warp's span
+    constexpr int LS = POS / V, JS = POS % V;
+    static_assert(TT > KX && TT >= 2 * KX, "feed records must be ordered by the exchange barriers");
+    const bool wr = warp == NW - 1;
+    own_ok = true;
+    int dn = 0;
+    for (int e = 0;; ++e) {
+        const int Ks = (TT - dn) < KX ? (TT - dn) : KX;
+        if (OPS == 1 && Ks == KX)
+            warp_steps_fd_fixed<V, OPS, LS, JS, KX>(u, r, dn, fin, fout, rd, wr, lane);
+        else
+            warp_steps_fd<V, OPS, LS, JS>(u, Ks, r, dn, fin, fout, rd, wr, lane);
+        dn += Ks;
+        if (dn >= TT) break;  // (TT > KX: the barrier of exchange 0 ordered every span load before)
+        double *X = xbuf + (size_t)(e & 1) * (NW * 2 * KX);
+        if (lane == 0 && warp > 0) {
+#pragma unroll
+            for (int i = 0; i < KX; ++i) X[(warp * 2 + 0) * KX + i] = u[KX + i];
+        }
+        if (lane == 31 && warp < NW - 1) {
+#pragma unroll
+            for (int i = 0; i < KX; ++i) X[(warp * 2 + 1) * KX + i] = u[V - 2 * KX + i];
+        }
+        if (GUARD && e == 0) {
+            own_ok = __shfl_sync(0xffffffffu, (int)bar1_and<NW * 32>(ok), 0) != 0;
+            if (!(own_ok && prev_ok)) return false;
+        } else {
+            asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+        }
+        if (lane == 0 && warp > 0) {
+#pragma unroll
+            for (int i = 0; i < KX; ++i) u[i] = X[((warp - 1) * 2 + 1) * KX + i];
+        }
+        if (lane == 31 && warp < NW - 1) {
+#pragma unroll
+            for (int i = 0; i < KX; ++i) u[V - KX + i] = X[((warp + 1) * 2 + 0) * KX + i];
+        }
+    }
+    if constexpr (ops_scaled(OPS)) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) u[j] = __dmul_rn(u[j], scale);
+    }
+    return true;
+}
+
+// write-back of a feed tile: warp 0 owns from position 0 when fed (else T), the last warp up
+// to 32V - TT (the right margin), inner sides exclude the KX ghost zones
+template <int V, int NW, int KX, int TT>
+__device__ __forceinline__ void write_back_fd(const double (&u)[V], double *st, int base, bool fed, int warp,
+                                              int lane) {
+    const int lo = warp == 0 ? (fed ? 0 : TT) : KX;
+    const int hi = warp == NW - 1 ? 32 * V - TT : 32 * V - KX;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        const int p = lane * V + j;
+        if (p >= lo && p < hi) st[base + j] = u[j];
+    }
+}
+
+template <int V, int NW, int KX, int TT>
+__device__ __noinline__ void tile_literal_fd(double *st, int base, double r, double *xbuf, const double *fin,
+                                             double *fout, bool fed, int warp, int lane) {
+    double u[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) u[j] = st[base + j];
+    bool dummy;
+    tile_steps_fd<V, NW, KX, 5, false, TT>(u, r, 1.0, xbuf, fin, fout, fed, warp, lane, true, true, dummy);
+    write_back_fd<V, NW, KX, TT>(u, st, base, fed, warp, lane);
+}
+
+// A CTA's strip [S0, S1) of the output and its tiles: the first with both T-deep margins
+// (window [x0 - TT, x1 + TT)), the rest fed on the left (window [x0, x1 + TT)).
+struct FdStrip {
+    int64_t S0 = 0, S1 = 0, W = 0, Ws = 0;
+    int64_t ntile = 0;
+    __device__ void tile(int64_t i, int64_t *x0, int64_t *x1, int64_t *win_lo) const {
+        *x0 = i == 0 ? S0 : S0 + W + (i - 1) * Ws;
+        const int64_t e = *x0 + (i == 0 ? W : Ws);
+        *x1 = e < S1 ? e : S1;
+        *win_lo = i == 0 ? *x0 - (Ws - W) : *x0;  // the first tile has a T-deep left margin (Ws - W = T)
+    }
+};
+
+template <int V, int NW, int KX, int TT>
+__device__ __forceinline__ FdStrip fd_strip(int64_t out_lo, int64_t out_hi) {
+    constexpr int64_t SPAN = (int64_t)NW * 32 * V - 2 * KX * (NW - 1);
+    FdStrip f;
+    f.W = SPAN - 2 * TT;
+    f.Ws = SPAN - TT;
+    const int64_t total = out_hi - out_lo;
+    const int64_t L = (total + gridDim.x - 1) / gridDim.x;
+    f.S0 = out_lo + (int64_t)blockIdx.x * L;
+    f.S1 = f.S0 + L < out_hi ? f.S0 + L : out_hi;
+    if (f.S0 >= f.S1) return f;
+    const int64_t len = f.S1 - f.S0;
+    f.ntile = len <= f.W ? 1 : 1 + (len - f.W + f.Ws - 1) / f.Ws;
+    return f;
+}
+
+// The compute warps' strip loop (OPS, coefficient r); also fast mode's 3-op fallback.
+template <int V, int NW, int S, int KX, int OPS, bool GUARD, int TT>
+__device__ __forceinline__ void compute_loop_fd(uint64_t *full, uint64_t *done, double *stages,
+                                                uint32_t stage_doubles, const FdStrip &f, double r, double scale,
+                                                Guard guard, double *xbuf, double *feed, int warp, int lane) {
+    const int SW = 32 * V - 2 * KX;
+    bool prev_ok = true;
+    for (int64_t i = 0; i < f.ntile; ++i) {
+        const int s = (int)(i % S);
+        double *st = stages + (size_t)s * stage_doubles;
+        int64_t x0, x1, wl;
+        f.tile(i, &x0, &x1, &wl);
+        const bool fed = i > 0;
+        mbar_wait_sleep(&full[s], (uint32_t)((i / S) & 1));
+        const int base = (int)(wl & 1) + warp * SW + lane * V;
+        HCHECK(base >= 0 && base + V <= (int)stage_doubles);
+        double u[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) u[j] = st[base + j];
+        bool ok = true;
+        if constexpr (GUARD) {
+            GuardAcc acc;
+#pragma unroll
+            for (int j = 0; j < V; ++j) acc.add(u[j]);
+            ok = acc.ok(guard);
+        }
+        const double *fin = feed + (size_t)((i + 1) & 1) * TT;  // written by tile i - 1
+        double *fout = feed + (size_t)(i & 1) * TT;
+        bool own_ok = true;
+        if (tile_steps_fd<V, NW, KX, OPS, GUARD, TT>(u, r, scale, xbuf, fin, fout, fed, warp, lane, ok, prev_ok,
+                                                     own_ok))
+            write_back_fd<V, NW, KX, TT>(u, st, base, fed, warp, lane);
+        else
+            tile_literal_fd<V, NW, KX, TT>(st, base, r, xbuf, fin, fout, fed, warp, lane);
+        prev_ok = own_ok;
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&done[s]);
+    }
+}
+
+template <int V, int NW, int S, int OPS, int KX, int TT>
+__global__ void __launch_bounds__((NW + 1) * 32, 2)
+k2f_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T, int64_t out_lo, int64_t out_hi,
+         int wrapT, double r, double scale, int64_t ntiles, uint32_t stage_doubles, Guard guard, FastRange fr) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);
+    uint64_t *done = full + S;
+    double *stages = reinterpret_cast<double *>(smem_raw + 128);
+    constexpr bool GUARD = ops_guarded(OPS);
+    (void)T;
+    (void)ntiles;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+    double *xbuf = stages + (size_t)S * stage_doubles;  // [2 parities][NW][2 sides][KX]
+    double *feed = xbuf + (size_t)2 * NW * 2 * KX;      // [2 tile parities][TT]
+    const FdStrip f = fd_strip<V, NW, KX, TT>(out_lo, out_hi);
+
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&done[s], NW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == NW) {
+        // ---------------- producer warp: the strip's tiles in order
+        const uint64_t pol_in = policy_evict_first();
+        auto span_of = [&](int64_t i, int64_t *x0, int64_t *x1, int64_t *ld_lo, int64_t *ld_hi) {
+            int64_t wl;
+            f.tile(i, x0, x1, &wl);
+            *ld_lo = wl - (wl & 1);
+            *ld_hi = *x1 + TT + ((*x1 + TT) & 1);
+        };
+        auto issue_load = [&](int64_t i, int s) {
+            int64_t x0, x1, ld_lo, ld_hi;
+            span_of(i, &x0, &x1, &ld_lo, &ld_hi);
+            const uint32_t bytes = (uint32_t)((ld_hi - ld_lo) * 8);
+            HCHECK(bytes <= stage_doubles * 8u);
+            HCHECK(ld_lo >= -(int64_t)TT - 1 && ld_hi <= n + TT + 1);
+            HCHECK((128 + (size_t)S * stage_doubles * 8 + (size_t)2 * NW * 2 * KX * 8 + (size_t)2 * TT * 8) <=
+                   dynamic_smem_bytes());
+            mbar_arrive_expect_tx(&full[s], bytes);
+            bulk_g2s(stages + (size_t)s * stage_doubles, A + ld_lo, bytes, &full[s], pol_in);
+        };
+        HCHECK(out_lo >= 0 && out_hi <= n && wrapT <= n && wrapT <= 128);
+        if (lane == 0)
+            for (int i = 0; i < S && i < f.ntile; ++i) issue_load(i, i);
+        for (int64_t i = 0; i < f.ntile; ++i) {
+            const int s = (int)(i % S);
+            double *st = stages + (size_t)s * stage_doubles;
+            int64_t x0, x1, ld_lo, ld_hi;
+            span_of(i, &x0, &x1, &ld_lo, &ld_hi);
+            mbar_wait_backoff(&done[s], (uint32_t)((i / S) & 1));
+            if (lane == 0 && (x0 & 1)) B[x0] = st[x0 - ld_lo];
+            if (lane == 1 && (x1 & 1) && x1 - 1 >= x0) B[x1 - 1] = st[x1 - 1 - ld_lo];
+            for (int j = lane; j < wrapT; j += 32) {
+                if (j >= x0 && j < x1) B[n + j] = st[j - ld_lo];
+                const int64_t c = n - wrapT + j;
+                if (c >= x0 && c < x1) B[j - wrapT] = st[c - ld_lo];
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const int64_t a = x0 + (x0 & 1);
+                const int64_t b = x1 - (x1 & 1);
+                if (b > a) bulk_s2g(B + a, st + (a - ld_lo), (uint32_t)((b - a) * 8));
+                bulk_commit();
+                if (i + S < f.ntile) {
+                    bulk_wait_read<0>();
+                    fence_proxy_async();
+                    issue_load(i + S, s);
+                }
+            }
+            __syncwarp();
+        }
+        if (lane == 0) bulk_wait<0>();
+        return;
+    }
+
+    // ---------------- compute warps
+    if constexpr (ops_scaled(OPS)) {
+        if (!__shfl_sync(0xffffffffu, (int)scaled_in_range(fr), 0)) {
+            compute_loop_fd<V, NW, S, KX, 3, false, TT>(full, done, stages, stage_doubles, f, fr.r, 1.0, guard, xbuf,
+                                                        feed, warp, lane);
+            return;
+        }
+    }
+    compute_loop_fd<V, NW, S, KX, OPS, GUARD, TT>(full, done, stages, stage_doubles, f, r, scale, guard, xbuf, feed,
+                                                  warp, lane);
+}
+
 size_t PassGeom::smem_bytes(int T) const {
     const int64_t in_cells = tile_out(T) + 2 * T + 2;
     const int64_t stage = (in_cells + 15) / 16 * 16;
     const size_t xch = (size_t)2 * NW * 2 * kx_of(kind) * sizeof(double);
-    return 128 + (size_t)S * (size_t)stage * sizeof(double) + xch;
+    const size_t feed = (size_t)2 * 128 * sizeof(double);  // k2f_pass's boundary records (T <= 128)
+    return 128 + (size_t)S * (size_t)stage * sizeof(double) + xch + feed;
 }
 
 namespace {
@@ -447,6 +744,36 @@ PassFn pass_fn_x(int ops) {
     }
 }
 
+// HEAT1D_NOFEED=1 (measurement knob, read once): every pass on k2p_pass
+bool feed_disabled() {
+    static const bool off = [] {
+        const char *e = getenv("HEAT1D_NOFEED");
+        return e && atoi(e) == 1;
+    }();
+    return off;
+}
+
+// feed tiles (k2f_pass): the default geometry at the auto T values and 128
+PassFn lookup_feed(const PassGeom &g, int ops, int T) {
+#ifdef HEAT1D_NOFEED
+    (void)g; (void)ops; (void)T;
+    return nullptr;
+#else
+    if (!(g.V == 51 && g.NW == 4 && g.S == 2 && g.kind == 4)) return nullptr;
+#define F(tt)                                                   \
+    if (T == tt) switch (ops) {                                 \
+            case 4: return &k2f_pass<51, 4, 2, 4, 16, tt>;      \
+            case 3: return &k2f_pass<51, 4, 2, 3, 16, tt>;      \
+            case 2: return &k2f_pass<51, 4, 2, 2, 16, tt>;      \
+            case 1: return &k2f_pass<51, 4, 2, 1, 16, tt>;      \
+            default: return nullptr;                            \
+        }
+    F(64) F(96) F(128)
+#undef F
+    return nullptr;
+#endif
+}
+
 PassFn lookup_pass(int V, int NW, int S, int ops, int kind) {
     if (kind != 3 && kind != 4) return nullptr;
 #define X(v, nw, s) \
@@ -459,6 +786,8 @@ PassFn lookup_pass(int V, int NW, int S, int ops, int kind) {
 }  // namespace
 
 bool pass_supported(const PassGeom &g, int ops) { return lookup_pass(g.V, g.NW, g.S, ops, g.kind) != nullptr; }
+
+bool pass_uses_feed(const PassGeom &g, int ops, int T) { return lookup_feed(g, ops, T) && !feed_disabled(); }
 
 PassGeom choose_geom(int64_t n_out, int T, int num_sms, int ops) {
     // Default (profiles/r01_sweep_kx.jsonl): CTA tiles of 4 compute warps x
@@ -478,6 +807,8 @@ cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, 
                         const FastRange &fr, int num_sms, cudaStream_t st, int *grid_out) {
     PassFn fn = lookup_pass(g.V, g.NW, g.S, ops, g.kind);
     if (!fn) return cudaErrorInvalidConfiguration;
+    PassFn ffn = lookup_feed(g, ops, T);
+    if (ffn && !feed_disabled()) fn = ffn;
     if (out_hi <= out_lo) {
         if (grid_out) *grid_out = 0;
         return cudaSuccess;
@@ -519,7 +850,7 @@ cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, 
         occ = 1;
     const int per_sm = g.ctas_per_sm < occ ? g.ctas_per_sm : occ;
     int64_t grid = (int64_t)num_sms * per_sm;
-    if (grid > units) grid = units;
+    if (grid > units) grid = units;  // (k2f_pass: strips of at least one first-tile width)
     if (grid_out) *grid_out = (int)grid;
     fn<<<(unsigned)grid, threads, smem, st>>>(A, B, n, T, out_lo, out_hi, wrapT, q, scale, units, stage_doubles,
                                              guard, fr);

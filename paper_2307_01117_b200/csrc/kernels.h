@@ -91,6 +91,9 @@ PassGeom choose_geom(int64_t n_out, int T, int num_sms, int ops);
 // B[n, n+wrapT) and cells [n-wrapT, n) to B[-wrapT, 0)  (periodic self-halo).
 // q = the variant's per-step coefficient, scale = r^T (scaled variants only; stencil.cuh),
 // guard = the exactness guard (guard_of; guarded variants only).
+// whether launch_pass runs a full pass of depth T as feed tiles (k2f_pass)
+bool pass_uses_feed(const PassGeom &g, int ops, int T);
+
 cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, int64_t n,
                         int T, int64_t out_lo, int64_t out_hi, int wrapT, double q, double scale,
                         Guard guard, const FastRange &fr, int num_sms, cudaStream_t st, int *grid_out);

@@ -89,6 +89,8 @@ class Info(ctypes.Structure):
         ("stream_windows", ctypes.c_int64),
         ("transport", ctypes.c_int32),
         ("resident_V", ctypes.c_int32),
+        ("pass_feed", ctypes.c_int32),
+        ("reserved1", ctypes.c_int32),
     ]
 
 
