@@ -282,6 +282,78 @@ __device__ __forceinline__ void compute_loop_fma3(uint64_t *full, uint64_t *done
     }
 }
 
+// The producer warp of a pass kernel: for the CTA's tiles i = 0 .. geo.count()-1 (geo.span(i):
+// output [x0, x1), 16-byte-aligned load window [ld_lo, ld_hi)), keep S TMA loads in flight,
+// and once the compute warps release a stage store its output (bulk, plus the scalar
+// leftovers: an odd first/last cell and the periodic self-halo of a single-slab ring).
+template <int S, int NW, int KX, class Geo>
+__device__ __forceinline__ void producer_loop(const Geo &geo, uint64_t *full, uint64_t *done, double *stages,
+                                              uint32_t stage_doubles, const double *__restrict__ A,
+                                              double *__restrict__ B, int64_t n, int wrapT, int halo, int feed_doubles,
+                                              int lane) {
+    const uint64_t pol_in = policy_evict_first();
+    const int64_t count = geo.count();
+    auto issue_load = [&](int64_t i, int s) {
+        int64_t x0, x1, ld_lo, ld_hi;
+        geo.span(i, &x0, &x1, &ld_lo, &ld_hi);
+        const uint32_t bytes = (uint32_t)((ld_hi - ld_lo) * 8);
+        HCHECK(bytes <= stage_doubles * 8u);                             // the stage holds the tile input
+        HCHECK(ld_lo >= -(int64_t)halo - 1 && ld_hi <= n + halo + 1);  // within the padded slab
+        HCHECK((128 + (size_t)S * stage_doubles * 8 + (size_t)2 * NW * 2 * KX * 8 + (size_t)feed_doubles * 8) <=
+               dynamic_smem_bytes());
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_g2s(stages + (size_t)s * stage_doubles, A + ld_lo, bytes, &full[s], pol_in);
+    };
+    HCHECK(wrapT <= n && wrapT <= 128);  // (wrapT: the pad fill, <= T_MAX)
+    if (lane == 0)
+        for (int i = 0; i < S && i < count; ++i) issue_load(i, i);
+    for (int64_t i = 0; i < count; ++i) {
+        const int s = (int)(i % S);
+        double *st = stages + (size_t)s * stage_doubles;
+        int64_t x0, x1, ld_lo, ld_hi;
+        geo.span(i, &x0, &x1, &ld_lo, &ld_hi);
+        mbar_wait_backoff(&done[s], (uint32_t)((i / S) & 1));
+        if (lane == 0 && (x0 & 1)) B[x0] = st[x0 - ld_lo];
+        if (lane == 1 && (x1 & 1) && x1 - 1 >= x0) B[x1 - 1] = st[x1 - 1 - ld_lo];
+        for (int j = lane; j < wrapT; j += 32) {
+            if (j >= x0 && j < x1) B[n + j] = st[j - ld_lo];
+            const int64_t c = n - wrapT + j;
+            if (c >= x0 && c < x1) B[j - wrapT] = st[c - ld_lo];
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const int64_t a = x0 + (x0 & 1);
+            const int64_t b = x1 - (x1 & 1);
+            if (b > a) bulk_s2g(B + a, st + (a - ld_lo), (uint32_t)((b - a) * 8));
+            bulk_commit();
+            if (i + S < count) {
+                bulk_wait_read<0>();  // the tile's bytes have left the stage
+                fence_proxy_async();
+                issue_load(i + S, s);
+            }
+        }
+        __syncwarp();
+    }
+    if (lane == 0) bulk_wait<0>();
+}
+
+// k2p_pass's tiles: round robin over the CTAs, both T-deep margins loaded
+struct RoundRobinTiles {
+    int64_t out_lo, out_hi, W, ntiles;
+    int T;
+    __device__ int64_t count() const {
+        return ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
+    }
+    __device__ void span(int64_t i, int64_t *x0, int64_t *x1, int64_t *ld_lo, int64_t *ld_hi) const {
+        const int64_t tile = (int64_t)blockIdx.x + i * gridDim.x;
+        *x0 = out_lo + tile * W;
+        *x1 = min(*x0 + W, out_hi);
+        const int64_t lo = *x0 - T;
+        *ld_lo = lo - (lo & 1);
+        *ld_hi = *x1 + T + ((*x1 + T) & 1);
+    }
+};
+
 // Register target: the occupancy choose_geom plans for (2 CTAs/SM; 4 for V <= 17 tiles).
 // Without it ptxas sizes the kernel for the guard's out-of-line fallback as well.
 template <int V, int NW, int S, int OPS, int KX>
@@ -312,65 +384,10 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
     }
     __syncthreads();
 
-    if (warp == NW) {
-        // ---------------- producer warp
-        const uint64_t pol_in = policy_evict_first();
-        auto span_of = [&](int64_t tile, int64_t *x0, int64_t *x1, int64_t *ld_lo, int64_t *ld_hi) {
-            *x0 = out_lo + tile * W;
-            *x1 = min(*x0 + W, out_hi);
-            const int64_t lo = *x0 - T;
-            *ld_lo = lo - (lo & 1);
-            *ld_hi = *x1 + T + ((*x1 + T) & 1);
-        };
-        auto issue_load = [&](int64_t tile, int s) {
-            int64_t x0, x1, ld_lo, ld_hi;
-            span_of(tile, &x0, &x1, &ld_lo, &ld_hi);
-            const uint32_t bytes = (uint32_t)((ld_hi - ld_lo) * 8);
-            HCHECK(bytes <= stage_doubles * 8u);                     // the stage holds the tile input
-            HCHECK(ld_lo >= -(int64_t)T - 1 && ld_hi <= n + T + 1);  // within the padded slab
-            HCHECK((128 + (size_t)S * stage_doubles * 8 + (size_t)2 * NW * 2 * KX * 8) <= dynamic_smem_bytes());
-            mbar_arrive_expect_tx(&full[s], bytes);
-            bulk_g2s(stages + (size_t)s * stage_doubles, A + ld_lo, bytes, &full[s], pol_in);
-        };
-        HCHECK(out_lo >= 0 && out_hi <= n && wrapT <= n && wrapT <= 128);  // (wrapT: the pad fill, <= T_MAX)
-        if (lane == 0) {
-            for (int i = 0; i < S; ++i) {
-                const int64_t tile = blockIdx.x + i * stride;
-                if (tile >= ntiles) break;
-                issue_load(tile, i);
-            }
-        }
-        int k = 0;
-        for (int64_t tile = blockIdx.x; tile < ntiles; tile += stride, ++k) {
-            const int s = k % S;
-            double *st = stages + (size_t)s * stage_doubles;
-            int64_t x0, x1, ld_lo, ld_hi;
-            span_of(tile, &x0, &x1, &ld_lo, &ld_hi);
-            mbar_wait_backoff(&done[s], (uint32_t)((k / S) & 1));
-            // scalar leftovers: an odd first/last cell and the periodic self-halo
-            if (lane == 0 && (x0 & 1)) B[x0] = st[x0 - ld_lo];
-            if (lane == 1 && (x1 & 1) && x1 - 1 >= x0) B[x1 - 1] = st[x1 - 1 - ld_lo];
-            for (int j = lane; j < wrapT; j += 32) {
-                if (j >= x0 && j < x1) B[n + j] = st[j - ld_lo];
-                const int64_t c = n - wrapT + j;
-                if (c >= x0 && c < x1) B[j - wrapT] = st[c - ld_lo];
-            }
-            __syncwarp();
-            if (lane == 0) {
-                const int64_t a = x0 + (x0 & 1);
-                const int64_t b = x1 - (x1 & 1);
-                if (b > a) bulk_s2g(B + a, st + (a - ld_lo), (uint32_t)((b - a) * 8));
-                bulk_commit();
-                const int64_t nxt = tile + (int64_t)S * stride;
-                if (nxt < ntiles) {
-                    bulk_wait_read<0>();  // tile's bytes have left the stage
-                    fence_proxy_async();
-                    issue_load(nxt, s);
-                }
-            }
-            __syncwarp();
-        }
-        if (lane == 0) bulk_wait<0>();
+    if (warp == NW) {  // ---------------- producer warp
+        HCHECK(out_lo >= 0 && out_hi <= n);
+        const RoundRobinTiles geo{out_lo, out_hi, W, ntiles, T};
+        producer_loop<S, NW, KX>(geo, full, done, stages, stage_doubles, A, B, n, wrapT, T, 0, lane);
         return;
     }
 
@@ -576,6 +593,19 @@ __device__ __forceinline__ FdStrip fd_strip(int64_t out_lo, int64_t out_hi) {
     return f;
 }
 
+// k2f_pass's tiles for the producer: the strip's, with their 16-byte-aligned load windows
+template <int TT>
+struct FdTilesT {
+    FdStrip f;
+    __device__ int64_t count() const { return f.ntile; }
+    __device__ void span(int64_t i, int64_t *x0, int64_t *x1, int64_t *ld_lo, int64_t *ld_hi) const {
+        int64_t wl;
+        f.tile(i, x0, x1, &wl);
+        *ld_lo = wl - (wl & 1);
+        *ld_hi = *x1 + TT + ((*x1 + TT) & 1);
+    }
+};
+
 // The compute warps' strip loop (OPS, coefficient r); also fast mode's 3-op fallback.
 template <int V, int NW, int S, int KX, int OPS, bool GUARD, int TT>
 __device__ __forceinline__ void compute_loop_fd(uint64_t *full, uint64_t *done, double *stages,
@@ -644,57 +674,9 @@ k2f_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
     }
     __syncthreads();
 
-    if (warp == NW) {
-        // ---------------- producer warp: the strip's tiles in order
-        const uint64_t pol_in = policy_evict_first();
-        auto span_of = [&](int64_t i, int64_t *x0, int64_t *x1, int64_t *ld_lo, int64_t *ld_hi) {
-            int64_t wl;
-            f.tile(i, x0, x1, &wl);
-            *ld_lo = wl - (wl & 1);
-            *ld_hi = *x1 + TT + ((*x1 + TT) & 1);
-        };
-        auto issue_load = [&](int64_t i, int s) {
-            int64_t x0, x1, ld_lo, ld_hi;
-            span_of(i, &x0, &x1, &ld_lo, &ld_hi);
-            const uint32_t bytes = (uint32_t)((ld_hi - ld_lo) * 8);
-            HCHECK(bytes <= stage_doubles * 8u);
-            HCHECK(ld_lo >= -(int64_t)TT - 1 && ld_hi <= n + TT + 1);
-            HCHECK((128 + (size_t)S * stage_doubles * 8 + (size_t)2 * NW * 2 * KX * 8 + (size_t)2 * TT * 8) <=
-                   dynamic_smem_bytes());
-            mbar_arrive_expect_tx(&full[s], bytes);
-            bulk_g2s(stages + (size_t)s * stage_doubles, A + ld_lo, bytes, &full[s], pol_in);
-        };
-        HCHECK(out_lo >= 0 && out_hi <= n && wrapT <= n && wrapT <= 128);
-        if (lane == 0)
-            for (int i = 0; i < S && i < f.ntile; ++i) issue_load(i, i);
-        for (int64_t i = 0; i < f.ntile; ++i) {
-            const int s = (int)(i % S);
-            double *st = stages + (size_t)s * stage_doubles;
-            int64_t x0, x1, ld_lo, ld_hi;
-            span_of(i, &x0, &x1, &ld_lo, &ld_hi);
-            mbar_wait_backoff(&done[s], (uint32_t)((i / S) & 1));
-            if (lane == 0 && (x0 & 1)) B[x0] = st[x0 - ld_lo];
-            if (lane == 1 && (x1 & 1) && x1 - 1 >= x0) B[x1 - 1] = st[x1 - 1 - ld_lo];
-            for (int j = lane; j < wrapT; j += 32) {
-                if (j >= x0 && j < x1) B[n + j] = st[j - ld_lo];
-                const int64_t c = n - wrapT + j;
-                if (c >= x0 && c < x1) B[j - wrapT] = st[c - ld_lo];
-            }
-            __syncwarp();
-            if (lane == 0) {
-                const int64_t a = x0 + (x0 & 1);
-                const int64_t b = x1 - (x1 & 1);
-                if (b > a) bulk_s2g(B + a, st + (a - ld_lo), (uint32_t)((b - a) * 8));
-                bulk_commit();
-                if (i + S < f.ntile) {
-                    bulk_wait_read<0>();
-                    fence_proxy_async();
-                    issue_load(i + S, s);
-                }
-            }
-            __syncwarp();
-        }
-        if (lane == 0) bulk_wait<0>();
+    if (warp == NW) {  // ---------------- producer warp: the strip's tiles in order
+        HCHECK(out_lo >= 0 && out_hi <= n);
+        producer_loop<S, NW, KX>(FdTilesT<TT>{f}, full, done, stages, stage_doubles, A, B, n, wrapT, TT, 2 * TT, lane);
         return;
     }
 
