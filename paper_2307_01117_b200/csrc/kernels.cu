@@ -256,13 +256,14 @@ __device__ __noinline__ void tile_literal(double *st, int base, int T, double r,
     write_back<V, NW, KX>(u, st, base, T, warp, lane);
 }
 
-// The compute warps' tile loop in the contracted 3-op form (coefficient r): fast mode's
-// fallback for a pass whose scaled state could overflow (FastRange).  Inlined as a disjoint
-// branch: a call (out of line) would constrain the hot loop's registers (-2 %).
-template <int V, int NW, int S, int KX>
-__device__ __forceinline__ void compute_loop_fma3(uint64_t *full, uint64_t *done, double *stages,
-                                               uint32_t stage_doubles, int64_t out_lo, int64_t W, int T, double r,
-                                               int64_t ntiles, double *xbuf, int warp, int lane) {
+// The compute warps' tile loop (OPS, coefficient r; fast mode's fallback for a pass whose scaled
+// state could overflow runs it with OPS 3 and r).  Inlined at both call sites as disjoint
+// branches: a call (out of line) would constrain the hot loop's registers (-2 %).
+template <int V, int NW, int S, int KX, int OPS, bool GUARD>
+__device__ __forceinline__ void compute_loop_rr(uint64_t *full, uint64_t *done, double *stages,
+                                                uint32_t stage_doubles, int64_t out_lo, int64_t W, int T, double r,
+                                                double scale, Guard guard, int64_t ntiles, double *xbuf, int warp,
+                                                int lane) {
     const int SW = 32 * V - 2 * KX;
     int k = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
@@ -271,11 +272,21 @@ __device__ __forceinline__ void compute_loop_fma3(uint64_t *full, uint64_t *done
         const int64_t x0 = out_lo + tile * W;
         mbar_wait_sleep(&full[s], (uint32_t)((k / S) & 1));
         const int base = (int)((x0 - T) & 1) + warp * SW + lane * V;
+        HCHECK(base >= 0 && base + V <= (int)stage_doubles);
         double u[V];
 #pragma unroll
         for (int j = 0; j < V; ++j) u[j] = st[base + j];
-        tile_steps<V, NW, KX, 3, false>(u, T, r, 1.0, xbuf, warp, lane, true);
-        write_back<V, NW, KX>(u, st, base, T, warp, lane);
+        bool ok = true;
+        if constexpr (GUARD) {
+            GuardAcc acc;
+#pragma unroll
+            for (int j = 0; j < V; ++j) acc.add(u[j]);
+            ok = acc.ok(guard);
+        }
+        if (tile_steps<V, NW, KX, OPS, GUARD>(u, T, r, scale, xbuf, warp, lane, ok))
+            write_back<V, NW, KX>(u, st, base, T, warp, lane);
+        else
+            tile_literal<V, NW, KX>(st, base, T, r, xbuf, warp, lane);
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&done[s]);
@@ -370,9 +381,7 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform for the compiler
-    const int SW = 32 * V - 2 * KX;                            // span stride
-    const int64_t W = (int64_t)NW * 32 * V - 2 * KX * (NW - 1) - 2 * T;
-    const int64_t stride = gridDim.x;
+    const int64_t W = (int64_t)NW * 32 * V - 2 * KX * (NW - 1) - 2 * T;  // output cells per tile
     double *xbuf = stages + (size_t)S * stage_doubles;  // [2 parities][NW][2 sides][KX]
 
     if (tid == 0) {
@@ -392,44 +401,18 @@ k2p_pass(const double *__restrict__ A, double *__restrict__ B, int64_t n, int T,
     }
 
     // ---------------- compute warps
-    // scaled fast forms whose state could overflow run the whole pass in the 3-op form, in a
-    // separate copy of this loop (no branch inside the hot loop below); the decision is
-    // CTA-uniform, broadcast so that ptxas sees it warp-uniform
+    // scaled fast forms whose state could overflow run the whole pass in the 3-op form (no
+    // branch inside the hot loop); the decision is CTA-uniform, broadcast so that ptxas sees
+    // it warp-uniform
     if constexpr (ops_scaled(OPS)) {
         if (!__shfl_sync(0xffffffffu, (int)scaled_in_range(fr), 0)) {
-            compute_loop_fma3<V, NW, S, KX>(full, done, stages, stage_doubles, out_lo, W, T, fr.r, ntiles, xbuf,
-                                            warp, lane);
+            compute_loop_rr<V, NW, S, KX, 3, false>(full, done, stages, stage_doubles, out_lo, W, T, fr.r, 1.0, guard,
+                                                    ntiles, xbuf, warp, lane);
             return;
         }
     }
-    int k = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += stride, ++k) {
-        const int s = k % S;
-        const uint32_t par = (uint32_t)((k / S) & 1);
-        double *st = stages + (size_t)s * stage_doubles;
-        const int64_t x0 = out_lo + tile * W;
-        const int sh = (int)((x0 - T) & 1);
-        mbar_wait_sleep(&full[s], par);
-        const int base = sh + warp * SW + lane * V;
-        HCHECK(base >= 0 && base + V <= (int)stage_doubles);
-        double u[V];
-#pragma unroll
-        for (int j = 0; j < V; ++j) u[j] = st[base + j];
-        bool ok = true;
-        if constexpr (GUARD) {
-            GuardAcc acc;
-#pragma unroll
-            for (int j = 0; j < V; ++j) acc.add(u[j]);
-            ok = acc.ok(guard);
-        }
-        if (tile_steps<V, NW, KX, OPS, GUARD>(u, T, r, scale, xbuf, warp, lane, ok))
-            write_back<V, NW, KX>(u, st, base, T, warp, lane);
-        else
-            tile_literal<V, NW, KX>(st, base, T, r, xbuf, warp, lane);
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&done[s]);
-    }
+    compute_loop_rr<V, NW, S, KX, OPS, GUARD>(full, done, stages, stage_doubles, out_lo, W, T, r, scale, guard, ntiles,
+                                              xbuf, warp, lane);
 }
 
 // ------------------------------------------------------------------ K2f: feed tiles
