@@ -1,8 +1,11 @@
 // kernels.cu -- sm_100a kernels of libheat1d.
 //
-//   K2 k2p_pass     T fused Jacobi steps of Eq. 2 per HBM pass (the hot kernel): TMA
-//                   producer warp, register-resident warp spans trading 16-deep (kind 4,
-//                   default) or 8-deep (kind 3, small slabs) ghost zones between warps
+//   K2 k2f_pass     T fused Jacobi steps of Eq. 2 per HBM pass (the hot kernel): TMA
+//                   producer warp, register-resident warp spans trading 16-deep ghost zones
+//                   between warps, CTAs walking strips of left-fed tiles (full passes at
+//                   T = 64/96/128 on the default geometry)
+//      k2p_pass     the same with round-robin tiles and both T-deep margins (other T, tail
+//                   passes; kind 3 = 8-deep exchanges for small slabs)
 //   K1 k1_naive     one step per launch, modular indexing (T = 1 baseline)
 //   K3 k3_edges     the two T-wide edge strips of a slab once its ghosts arrived
 //   K3p k3_edges_put  K3 fused with the halo put into the neighbours' pads (P2P
