@@ -214,3 +214,26 @@ def test_nonfinite_inputs(h1, resident):
     got, _ = run_gpu(h1, u0, nt, 0.5, T=T, resident=resident)
     assert_same(got, want, "non-finite u0 resident=%s" % resident)
     assert np.isnan(want).sum() > 0 and np.isfinite(want).sum() > N // 2
+
+
+@pytest.mark.parametrize("recipe", ["planted", "straddle", "subnormal", "huge1023"])
+@pytest.mark.parametrize("mode", ["matched", "fast"])
+def test_feed_tiles_extremes(h1, recipe, mode):
+    """K2 feed tiles (k2f_pass) on a ring large enough for several left-fed tiles per CTA strip,
+    at the auto T (128), extreme magnitudes: a tile takes the contracted form only if its own
+    cells and the previous tile's passed the guard (the fed boundary depends on both), so planted
+    subnormals make their tile AND the next one fall back.  Matched: bitwise; fast mode (the
+    normal-range planted recipe only): within the north_star bound."""
+    if mode == "fast" and recipe not in ("planted",):
+        pytest.skip("the fast-mode bound is relative to normal-range states")
+    N = (1 << 22) + 12345
+    nt = 2 * 128 + 5
+    u0 = RECIPES[recipe](N)
+    want = oracle.run(u0, 0.5, nt)
+    got, info = run_gpu(h1, u0, nt, 0.5, resident=False, mode=mode)
+    assert info["T"] == 128 and info["pass_feed"] == 1
+    if mode == "matched":
+        assert_same(got, want, "feed tiles %s" % recipe)
+    else:
+        bound = 1e-12 * float(np.max(np.abs(u0))) * nt
+        assert float(np.max(np.abs(got - want))) <= bound
