@@ -941,3 +941,19 @@ def test_resident_tag_counters_wrap(h1, monkeypatch, mailbox):
             h.run(nt)
             want = oracle.run(want, 0.5, nt)
             assert_bitwise(h.get(), want, "tags across the wrap, mailbox=%s nt=%d" % (mailbox, nt))
+
+
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_feed_tiles_multi_slab_interior(h1, transport):
+    """Two slabs of ~4M cells each at the auto T (128): every slab's interior pass [T, n - T) runs
+    as feed-tile strips of several tiles per CTA, next to the edge strips on the comm stream;
+    bitwise equal to the oracle after two full passes and a tail."""
+    nx = (1 << 22) + 1001
+    N, nt = 2 * nx, 2 * 128 + 7
+    u0 = synth.uniform(77, 0, N, -1.0, 1.0)
+    with h1.Heat1D(nx, 2, nt, 0.5, 1.0, 1.0, virtual_slabs=2, transport=transport) as h:
+        h.set_initial(u0)
+        h.run(nt)
+        info = h.info()
+        assert info["T"] == 128 and info["pass_feed"] == 1
+        assert_bitwise(h.get(), oracle.run(u0, 0.5, nt), "feed strips, 2 slabs, %s" % transport)
