@@ -957,3 +957,24 @@ def test_feed_tiles_multi_slab_interior(h1, transport):
         info = h.info()
         assert info["T"] == 128 and info["pass_feed"] == 1
         assert_bitwise(h.get(), oracle.run(u0, 0.5, nt), "feed strips, 2 slabs, %s" % transport)
+
+
+@pytest.mark.parametrize("T", [64, 96, 128])
+@pytest.mark.parametrize("k,mode", [(0.5, "matched"), (0.4, "matched"), (0.5, "fast"), (0.4, "fast")])
+def test_feed_tiles_every_depth(h1, T, k, mode):
+    """k2f_pass at each instantiated depth with several tiles per strip (4M cells: ~14 k cells per
+    CTA strip), 3-op / 4-op matched bitwise, 1-op / 2-op fast within the north_star bound."""
+    N = (1 << 22) + 777
+    nt = 2 * T + 3
+    u0 = synth.uniform(31 + T, 0, N, -1.0, 1.0)
+    with h1.Heat1D(N, 1, nt, k, 1.0, 1.0, T=T, mode=mode, resident=False) as h:
+        h.set_initial(u0)
+        h.run(nt)
+        info = h.info()
+        assert info["pass_feed"] == 1 and info["T"] == T
+        got = h.get()
+    want = oracle.run(u0, k, nt)
+    if mode == "matched":
+        assert_bitwise(got, want, "feed T=%d k=%g" % (T, k))
+    else:
+        assert float(np.max(np.abs(got - want))) <= 1e-12 * float(np.max(np.abs(u0))) * nt
