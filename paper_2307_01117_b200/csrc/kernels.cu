@@ -19,7 +19,6 @@
 // ghost zones.  The arithmetic is stencil.cuh; DESIGN.md §6
 // describes the data layout and the roofline of each kernel.
 #include <cstdio>
-#include <cstdlib>
 #include <cstdint>
 #include <mutex>
 
@@ -712,16 +711,7 @@ PassFn pass_fn_x(int ops) {
     }
 }
 
-// HEAT1D_NOFEED=1 (measurement knob, read once): every pass on k2p_pass
-bool feed_disabled() {
-    static const bool off = [] {
-        const char *e = getenv("HEAT1D_NOFEED");
-        return e && atoi(e) == 1;
-    }();
-    return off;
-}
-
-// feed tiles (k2f_pass): the default geometry at the auto T values and 128
+// feed tiles (k2f_pass): the default geometry at T = 64 / 96 / 128 (-DHEAT1D_NOFEED: never; A/B builds)
 PassFn lookup_feed(const PassGeom &g, int ops, int T) {
 #ifdef HEAT1D_NOFEED
     (void)g; (void)ops; (void)T;
@@ -755,7 +745,7 @@ PassFn lookup_pass(int V, int NW, int S, int ops, int kind) {
 
 bool pass_supported(const PassGeom &g, int ops) { return lookup_pass(g.V, g.NW, g.S, ops, g.kind) != nullptr; }
 
-bool pass_uses_feed(const PassGeom &g, int ops, int T) { return lookup_feed(g, ops, T) && !feed_disabled(); }
+bool pass_uses_feed(const PassGeom &g, int ops, int T) { return lookup_feed(g, ops, T) != nullptr; }
 
 PassGeom choose_geom(int64_t n_out, int T, int num_sms, int ops) {
     // Default (profiles/r01_sweep_kx.jsonl): CTA tiles of 4 compute warps x
@@ -775,8 +765,7 @@ cudaError_t launch_pass(const PassGeom &g, int ops, const double *A, double *B, 
                         const FastRange &fr, int num_sms, cudaStream_t st, int *grid_out) {
     PassFn fn = lookup_pass(g.V, g.NW, g.S, ops, g.kind);
     if (!fn) return cudaErrorInvalidConfiguration;
-    PassFn ffn = lookup_feed(g, ops, T);
-    if (ffn && !feed_disabled()) fn = ffn;
+    if (PassFn ffn = lookup_feed(g, ops, T)) fn = ffn;
     if (out_hi <= out_lo) {
         if (grid_out) *grid_out = 0;
         return cudaSuccess;
